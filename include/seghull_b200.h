@@ -1,0 +1,159 @@
+/*
+ * seghull_b200.h -- C-ABI of the B200-native 2D QuickHull (sm_100a).
+ *
+ * Drop-in boundary for the reference's hot path
+ *     seghull::hull::HullResult seghull::hull::run(const PointSet&, Mode, Backend)
+ *     (/root/reference/proj/core/include/seghull/hull.hpp:95,
+ *      /root/reference/proj/core/src/hull.cpp:219-290)
+ * The reference has no FFI of its own; this header is what its C++ `run`
+ * binds when a maintainer adds `Backend::B200` (INTEGRATION.md shows the
+ * patch).  Plain pointers and sizes only -- no C++ or torch types.
+ *
+ * Semantics (bit-exact with the reference):
+ *   - the output is the hull CCW from the leftmost vertex (ties: lowest y),
+ *     no repeated vertex, no collinear boundary point (hull.hpp:53-59);
+ *   - coordinates are returned bit-for-bit, plus the canonical input index of
+ *     each vertex: the lowest index among inputs with those coordinates;
+ *   - per-round SegmentStats equal the reference's (hull.hpp:35-40);
+ *   - orientation predicates are FP64 without contraction (-fmad=false).
+ *
+ * Errors mirror seghull::Errc (error.hpp:8-19): the return value is 0 or
+ * 1 + Errc; SH_CAP_TOO_SMALL sets *out_h to the required capacity;
+ * SH_CUDA_ERROR reports a CUDA runtime failure (message in `err`).
+ * Thread safety: re-entrant; every call uses a workspace taken from a
+ * per-device pool under a mutex ("independent run() calls may
+ * proceed in parallel").
+ */
+#ifndef SEGHULL_B200_H
+#define SEGHULL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SH_B200_ABI_VERSION 1
+
+/* return codes: 0 or 1 + seghull::Errc (error.hpp:8-19) */
+enum sh_status {
+  SH_OK = 0,
+  SH_EMPTY_INPUT = 1,         /* Errc::EmptyInput      hull.cpp:221      */
+  SH_NON_FINITE_INPUT = 2,    /* Errc::NonFiniteInput  hull.cpp:222-227  */
+  SH_DEGENERATE_INPUT = 3,    /* Errc::DegenerateInput hull.cpp:108-110  */
+  SH_INPUT_TOO_LARGE = 4,     /* Errc::InputTooLarge   (n >= 2^32 here)  */
+  SH_INTERNAL_ERROR = 5,      /* Errc::InternalError   hull.cpp:265-267  */
+  SH_CAP_TOO_SMALL = 100,     /* out buffers too small; *out_h = needed  */
+  SH_CUDA_ERROR = 101,        /* CUDA runtime error (no device, OOM, ...) */
+  SH_INVALID_ARGUMENT = 102
+};
+
+/* hull.hpp:48-51 Mode */
+enum sh_mode { SH_MODE_WITH_PREPROCESS = 1, SH_MODE_WITHOUT_PREPROCESS = 2 };
+
+/* flags */
+enum sh_flags {
+  SH_HOST_PTRS = 0u,      /* x, y (and idx) are host memory: H2D inside the call   */
+  SH_DEVICE_PTRS = 1u,    /* x, y (and idx) are device memory on `device`          */
+  SH_PHASE_TIMINGS = 2u,  /* record CUDA events per phase into sh_phase_ms         */
+  SH_NO_STATS = 4u        /* skip the per-round stats read-back                    */
+};
+
+/* hull.hpp:35-40 SegmentStats */
+typedef struct {
+  uint64_t iteration;
+  uint64_t segments;
+  uint64_t points_remaining;
+  uint64_t points_removed;
+} sh_round_stat;
+
+/* hull.hpp:42-46 PhaseTimings (device time from CUDA events) */
+typedef struct {
+  double pre_ms;      /* extremes + quadrilateral filter + chain classification */
+  double split_ms;    /* first split: round-1 routing of the filtered set         */
+  double recurse_ms;  /* remaining rounds until only hull vertices remain         */
+  double total_ms;    /* whole call on the device, H2D/D2H included when HOST_PTRS */
+} sh_phase_ms;
+
+/*
+ * Convex hull of (x[i], y[i]), i < n.  Equivalent of
+ * seghull::hull::run(points, Mode(mode), Backend::B200).
+ *   out_idx/out_x/out_y : caller-owned, capacity `cap` vertices (any may be NULL)
+ *   out_h               : number of hull vertices
+ *   stats/stats_cap     : per-round SegmentStats (may be NULL)
+ *   out_rounds          : number of refinement rounds executed (may be NULL)
+ *   phases              : per-phase device times (may be NULL; needs SH_PHASE_TIMINGS)
+ *   err/errlen          : message buffer (may be NULL)
+ */
+int sh_b200_hull(const double* x, const double* y, uint64_t n, int mode, uint32_t flags,
+                 int device, int64_t* out_idx, double* out_x, double* out_y, uint64_t cap,
+                 uint64_t* out_h, sh_round_stat* stats, uint64_t stats_cap,
+                 uint64_t* out_rounds, sh_phase_ms* phases, char* err, size_t errlen);
+
+/* Extended request: caller stream and caller-supplied point ids. */
+typedef struct {
+  const double* x;
+  const double* y;
+  uint64_t n;
+  const uint32_t* ids;  /* optional: id of each point (tie-break + output index);
+                           NULL means ids are 0..n-1.  Used by the shard merge,
+                           where ids are global input indices.                  */
+  int mode;
+  uint32_t flags;
+  int device;
+  void* stream;         /* cudaStream_t on `device`, or NULL for a pool stream   */
+} sh_hull_request;
+
+typedef struct {
+  int64_t* idx;
+  double* x;
+  double* y;
+  uint64_t cap;
+  uint64_t h;
+  sh_round_stat* stats;
+  uint64_t stats_cap;
+  uint64_t rounds;
+  uint64_t kept;        /* points surviving the Mode-1 filter (n in Mode 2)      */
+  uint64_t bad_index;   /* first non-finite index when SH_NON_FINITE_INPUT       */
+  sh_phase_ms phases;
+  uint32_t kernel_launches; /* kernels this call launched (evidence of GPU work) */
+  char err[256];
+} sh_hull_result;
+
+int sh_b200_hull_ex(const sh_hull_request* req, sh_hull_result* res);
+
+/*
+ * Device generators, bit-identical to the
+ * reference's host generators: SplitMix64 is counter-based, so point i of
+ * gen_uniform(n_total, seed) is x = draw(2i+1), y = draw(2i+2)
+ * (dataio.hpp:44-58, dataio.cpp:291-301).  Writes points
+ * [first, first + count) of the stream into device arrays x, y.
+ */
+int sh_b200_gen_uniform(double* x, double* y, uint64_t first, uint64_t count, uint64_t seed,
+                        int device, void* stream);
+
+/* Device twin of the disk generator defined in SURVEY.md section 8d
+ * (one stream, candidates (2u-1, 2v-1), accept iff x*x + y*y < 1 without FMA).
+ * Produces the first n accepted points; returns SH_OK. */
+int sh_b200_gen_disk(double* x, double* y, uint64_t n, uint64_t seed, int device, void* stream);
+
+/* Host twin of gen_circle (dataio.cpp:303-312): angle = 2*pi*u, (cos, sin)
+ * from the host libm, because device cos/sin are not bit-identical to glibc.
+ * Circle inputs are therefore generated on the host and uploaded. */
+int sh_b200_gen_circle_host(double* x, double* y, uint64_t n, uint64_t seed);
+
+/* Library/device information; returns SH_OK or SH_CUDA_ERROR. */
+int sh_b200_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
+                        uint64_t* hbm_bytes, char* name, size_t namelen);
+
+/* Release every pooled workspace on every device. */
+void sh_b200_release_pool(void);
+
+/* ABI version (SH_B200_ABI_VERSION). */
+int sh_b200_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEGHULL_B200_H */

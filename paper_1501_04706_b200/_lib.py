@@ -1,0 +1,78 @@
+"""ctypes binding of libseghull_b200.so (include/seghull_b200.h).
+
+The shared library is built in-tree by ``paper_1501_04706_b200.build`` (nvcc,
+sm_100a).  There is deliberately no fallback: if the library is missing the
+import of any compute entry point raises, so a GPU test can never pass on a
+silent CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libseghull_b200.so")
+
+_u64 = ctypes.c_uint64
+_u32 = ctypes.c_uint32
+_vp = ctypes.c_void_p
+
+
+class sh_round_stat(ctypes.Structure):
+    _fields_ = [("iteration", _u64), ("segments", _u64),
+                ("points_remaining", _u64), ("points_removed", _u64)]
+
+
+class sh_phase_ms(ctypes.Structure):
+    _fields_ = [("pre_ms", ctypes.c_double), ("split_ms", ctypes.c_double),
+                ("recurse_ms", ctypes.c_double), ("total_ms", ctypes.c_double)]
+
+
+class sh_hull_request(ctypes.Structure):
+    _fields_ = [("x", _vp), ("y", _vp), ("n", _u64), ("ids", _vp), ("mode", ctypes.c_int),
+                ("flags", _u32), ("device", ctypes.c_int), ("stream", _vp)]
+
+
+class sh_hull_result(ctypes.Structure):
+    _fields_ = [("idx", _vp), ("x", _vp), ("y", _vp), ("cap", _u64), ("h", _u64),
+                ("stats", _vp), ("stats_cap", _u64), ("rounds", _u64), ("kept", _u64),
+                ("bad_index", _u64), ("phases", sh_phase_ms), ("kernel_launches", _u32),
+                ("err", ctypes.c_char * 256)]
+
+
+# every symbol include/seghull_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = ("sh_b200_hull", "sh_b200_hull_ex", "sh_b200_gen_uniform", "sh_b200_gen_disk",
+           "sh_b200_gen_circle_host", "sh_b200_device_info", "sh_b200_release_pool",
+           "sh_b200_abi_version")
+
+SH_HOST_PTRS = 0
+SH_DEVICE_PTRS = 1
+SH_PHASE_TIMINGS = 2
+SH_NO_STATS = 4
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the CUDA library; raise loudly if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+    L = ctypes.CDLL(LIB_PATH)
+    L.sh_b200_hull.argtypes = [_vp, _vp, _u64, ctypes.c_int, _u32, ctypes.c_int, _vp, _vp, _vp,
+                               _u64, _vp, _vp, _u64, _vp, _vp, ctypes.c_char_p, ctypes.c_size_t]
+    L.sh_b200_hull_ex.argtypes = [ctypes.POINTER(sh_hull_request), ctypes.POINTER(sh_hull_result)]
+    L.sh_b200_gen_uniform.argtypes = [_vp, _vp, _u64, _u64, _u64, ctypes.c_int, _vp]
+    L.sh_b200_gen_disk.argtypes = [_vp, _vp, _u64, _u64, ctypes.c_int, _vp]
+    L.sh_b200_gen_circle_host.argtypes = [_vp, _vp, _u64, _u64]
+    L.sh_b200_device_info.argtypes = [ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_char_p,
+                                      ctypes.c_size_t]
+    L.sh_b200_release_pool.argtypes = []
+    L.sh_b200_release_pool.restype = None
+    L.sh_b200_abi_version.restype = ctypes.c_int
+    _lib = L
+    return L

@@ -1,0 +1,594 @@
+// seghull_b200.cu -- host orchestration and the C-ABI (include/seghull_b200.h).
+//
+// One call = one device-resident pipeline on one stream:
+//   [H2D] -> K1 -> K2 -> K3<first> -> { K4 -> K3 }* -> D2H(result)
+// Round bookkeeping lives in the device control block; the host only polls
+// the status word between batches of rounds (no per-round host logic).
+// Workspaces (all device buffers + pinned staging + events) are pooled per
+// device under a mutex, so repeated calls allocate nothing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/seghull_b200.h"
+#include "hull_kernels.cuh"
+
+namespace shb {
+size_t k3_smem_bytes();
+cudaError_t configure_kernels();
+int k3_blocks_per_sm();
+void launch_k1(const Bufs& B, int grid, cudaStream_t s);
+void launch_k2(const Bufs& B, bool filter, int grid, int reverse, cudaStream_t s);
+void launch_k3(const Bufs& B, bool first, int grid, cudaStream_t s);
+void launch_k4(const Bufs& B, int grid, cudaStream_t s);
+void launch_gen_uniform(double* x, double* y, unsigned long long first, unsigned long long count,
+                        unsigned long long seed, int grid, cudaStream_t s);
+void launch_gen_disk(double* x, double* y, unsigned long long n, unsigned long long seed,
+                     unsigned long long cand0, uint32_t ncand, unsigned long long out_base,
+                     Ctl* c, unsigned long long* status, uint32_t* epoch, int grid,
+                     cudaStream_t s);
+}  // namespace shb
+
+using namespace shb;
+
+namespace {
+
+struct CudaFail {
+  cudaError_t err;
+  const char* what;
+};
+
+#define CK(call)                                      \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) throw CudaFail{e_, #call}; \
+  } while (0)
+
+struct DeviceInfo {
+  int sm_count = 0;
+  bool configured = false;
+  int k3_bps = 1;
+};
+
+std::mutex g_mutex;
+std::vector<DeviceInfo> g_dev;
+
+struct Workspace {
+  int device = 0;
+  uint64_t n_cap = 0, s_cap = 0;
+  bool has_stage = false, has_stage_ids = false;
+  cudaStream_t stream = nullptr;
+  void* arena = nullptr;
+  void* stage = nullptr;
+  Bufs B{};
+  uint32_t* epoch = nullptr;
+  Ctl* h_ctl = nullptr;        // pinned
+  StatRec* h_stats = nullptr;  // pinned
+  cudaEvent_t ev[5] = {};
+  size_t tiles_cap = 0;
+  int k1_grid = 0, k2_grid = 0, k3_grid = 0, k4_grid = 0;
+
+  ~Workspace() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    if (arena) cudaFree(arena);
+    if (stage) cudaFree(stage);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_stats) cudaFreeHost(h_stats);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    cudaSetDevice(cur);
+  }
+};
+
+std::vector<std::vector<std::unique_ptr<Workspace>>> g_pool;  // free workspaces per device
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+DeviceInfo& device_info(int device) {
+  if ((int)g_dev.size() <= device) g_dev.resize(device + 1);
+  DeviceInfo& d = g_dev[device];
+  if (!d.configured) {
+    CK(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, device));
+    CK(configure_kernels());
+    d.k3_bps = k3_blocks_per_sm();
+    d.configured = true;
+  }
+  return d;
+}
+
+uint64_t seg_capacity(uint64_t n) {
+  if (n + 2 <= (1ull << 27)) return n + 2;
+  return std::max<uint64_t>(1ull << 27, n / 8);
+}
+
+std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s_cap) {
+  auto ws = std::make_unique<Workspace>();
+  ws->device = device;
+  ws->n_cap = n_cap;
+  ws->s_cap = s_cap;
+  DeviceInfo& di = device_info(device);
+  CK(cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking));
+  for (auto& e : ws->ev) CK(cudaEventCreate(&e));
+  CK(cudaMallocHost((void**)&ws->h_ctl, sizeof(Ctl)));
+  CK(cudaMallocHost((void**)&ws->h_stats, sizeof(StatRec) * STATS_CAP));
+
+  const uint64_t N = std::max<uint64_t>(n_cap, 64), S = std::max<uint64_t>(s_cap, 64);
+  ws->k1_grid = (int)std::min<uint64_t>((N + TPB - 1) / TPB, (uint64_t)di.sm_count * 8);
+  ws->k2_grid = ws->k1_grid;
+  ws->k3_grid = di.sm_count * di.k3_bps;
+  ws->k4_grid = di.sm_count * 4;
+  ws->tiles_cap = std::max<uint64_t>((N + TILE - 1) / TILE, (S + 2047) / 2048) + 64;
+
+  // carve one arena
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_ctl = take(sizeof(Ctl));
+  const size_t o_epoch = take(sizeof(uint32_t));
+  const size_t o_k1 = take(sizeof(K1Partial) * ws->k1_grid);
+  const size_t o_stats = take(sizeof(StatRec) * STATS_CAP);
+  const size_t o_tiles = take(sizeof(unsigned long long) * ws->tiles_cap);
+  const size_t words = (N + 31) / 32;
+  const size_t o_blo = take(4 * words), o_bup = take(4 * words);
+  size_t o_lx[2], o_ly[2], o_lid[2], o_lseg[2], o_tx[2], o_ty[2], o_tid[2], o_sd[2], o_sw[2];
+  for (int p = 0; p < 2; ++p) {
+    o_lx[p] = take(8 * N);
+    o_ly[p] = take(8 * N);
+    o_lid[p] = take(4 * N);
+    o_lseg[p] = take(4 * N);
+  }
+  for (int p = 0; p < 2; ++p) {
+    o_tx[p] = take(8 * S);
+    o_ty[p] = take(8 * S);
+    o_tid[p] = take(4 * S);
+    o_sd[p] = take(8 * S);
+    o_sw[p] = take(4 * S);
+  }
+  const size_t o_route = take(sizeof(Route) * S);
+  CK(cudaMalloc(&ws->arena, off));
+  char* a = (char*)ws->arena;
+  CK(cudaMemset(a, 0, o_tiles + sizeof(unsigned long long) * ws->tiles_cap));
+  Bufs& B = ws->B;
+  B.ctl = (Ctl*)(a + o_ctl);
+  ws->epoch = B.epoch = (uint32_t*)(a + o_epoch);
+  const uint32_t one = 1;
+  CK(cudaMemcpy(ws->epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
+  B.k1part = (K1Partial*)(a + o_k1);
+  B.stats = (StatRec*)(a + o_stats);
+  B.tile_status = (unsigned long long*)(a + o_tiles);
+  B.bits_lo = (uint32_t*)(a + o_blo);
+  B.bits_up = (uint32_t*)(a + o_bup);
+  for (int p = 0; p < 2; ++p) {
+    B.Lx[p] = (double*)(a + o_lx[p]);
+    B.Ly[p] = (double*)(a + o_ly[p]);
+    B.Lid[p] = (uint32_t*)(a + o_lid[p]);
+    B.Lseg[p] = (uint32_t*)(a + o_lseg[p]);
+    B.Tx[p] = (double*)(a + o_tx[p]);
+    B.Ty[p] = (double*)(a + o_ty[p]);
+    B.Tid[p] = (uint32_t*)(a + o_tid[p]);
+    B.Sd[p] = (unsigned long long*)(a + o_sd[p]);
+    B.Sw[p] = (uint32_t*)(a + o_sw[p]);
+  }
+  B.route = (Route*)(a + o_route);
+  B.s_cap = (uint32_t)std::min<uint64_t>(s_cap, 0xFFFFFFF0ull);
+  return ws;
+}
+
+void ensure_stage(Workspace& ws, bool ids) {
+  if (ws.has_stage && (!ids || ws.has_stage_ids)) return;
+  if (ws.stage) CK(cudaFree(ws.stage));
+  ws.stage = nullptr;
+  const size_t bytes = 16 * ws.n_cap + (ids ? 4 * ws.n_cap : 0) + 256;
+  CK(cudaMalloc(&ws.stage, bytes));
+  ws.has_stage = true;
+  ws.has_stage_ids = ids;
+}
+
+std::unique_ptr<Workspace> acquire(int device, uint64_t n) {
+  {
+    std::lock_guard<std::mutex> lk(g_mutex);
+    if ((int)g_pool.size() <= device) g_pool.resize(device + 1);
+    auto& v = g_pool[device];
+    int best = -1;
+    for (size_t i = 0; i < v.size(); ++i)
+      if (v[i]->n_cap >= n && (best < 0 || v[i]->n_cap < v[best]->n_cap)) best = (int)i;
+    if (best >= 0) {
+      auto ws = std::move(v[best]);
+      v.erase(v.begin() + best);
+      return ws;
+    }
+    device_info(device);
+  }
+  const uint64_t cap = std::max<uint64_t>(n, 1u << 12);
+  try {
+    return make_workspace(device, cap, seg_capacity(cap));
+  } catch (const CudaFail&) {
+    // out of memory: drop every pooled workspace on this device and retry once
+    cudaGetLastError();
+    {
+      std::lock_guard<std::mutex> lk(g_mutex);
+      g_pool[device].clear();
+    }
+    return make_workspace(device, cap, seg_capacity(cap));
+  }
+}
+
+void release(std::unique_ptr<Workspace> ws) {
+  std::lock_guard<std::mutex> lk(g_mutex);
+  if ((int)g_pool.size() <= ws->device) g_pool.resize(ws->device + 1);
+  auto& v = g_pool[ws->device];
+  v.push_back(std::move(ws));
+  if (v.size() > 3) {  // keep the pool bounded: drop the smallest workspace
+    size_t small = 0;
+    for (size_t i = 1; i < v.size(); ++i)
+      if (v[i]->n_cap < v[small]->n_cap) small = i;
+    v.erase(v.begin() + small);
+  }
+}
+
+void put_err(char* err, size_t len, const std::string& s) {
+  if (!err || !len) return;
+  std::snprintf(err, len, "%s", s.c_str());
+}
+
+struct RunOut {
+  int code = SH_OK;
+  uint64_t h = 0, rounds = 0, kept = 0, bad = 0;
+  uint32_t launches = 0;
+  std::string msg;
+};
+
+// Runs the pipeline; results stay in the workspace (h_ctl / device tables).
+RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, cudaStream_t st, bool timings,
+                    sh_phase_ms* ph) {
+  RunOut out;
+  Bufs B = ws.B;
+  const uint64_t n = rq.n;
+  const bool host = !(rq.flags & SH_DEVICE_PTRS);
+  if (timings) CK(cudaEventRecord(ws.ev[0], st));
+  if (host) {
+    ensure_stage(ws, rq.ids != nullptr);
+    B = ws.B;
+    double* sx = (double*)ws.stage;
+    double* sy = sx + ws.n_cap;
+    uint32_t* sid = (uint32_t*)(sy + ws.n_cap);
+    CK(cudaMemcpyAsync(sx, rq.x, 8 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(sy, rq.y, 8 * n, cudaMemcpyHostToDevice, st));
+    if (rq.ids) CK(cudaMemcpyAsync(sid, rq.ids, 4 * n, cudaMemcpyHostToDevice, st));
+    B.in_x = sx;
+    B.in_y = sy;
+    B.in_id = rq.ids ? sid : nullptr;
+  } else {
+    B.in_x = rq.x;
+    B.in_y = rq.y;
+    B.in_id = rq.ids;
+  }
+  B.n = (uint32_t)n;
+
+  Ctl init;
+  std::memset(&init, 0, sizeof(init));
+  init.status = ST_RUNNING;
+  init.n = (uint32_t)n;
+  init.s_cap = B.s_cap;
+  init.mode = (uint32_t)rq.mode;
+  *ws.h_ctl = init;
+  CK(cudaMemcpyAsync(B.ctl, ws.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+
+  const int g1 = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + TPB - 1) / TPB, ws.k1_grid));
+  launch_k1(B, g1, st);
+  launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, g1, /*reverse=*/1, st);
+  if (timings) CK(cudaEventRecord(ws.ev[1], st));
+  launch_k3(B, true, ws.k3_grid, st);
+  out.launches = 3;
+  if (timings) CK(cudaEventRecord(ws.ev[2], st));
+  CK(cudaGetLastError());
+
+  // rounds >= 2 in growing batches; each kernel exits at once when the
+  // device status is no longer RUNNING, so over-launching is harmless.
+  int batch = 6;
+  while (true) {
+    CK(cudaMemcpyAsync(ws.h_ctl, B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (ws.h_ctl->status != ST_RUNNING) break;
+    for (int k = 0; k < batch; ++k) {
+      launch_k4(B, ws.k4_grid, st);
+      launch_k3(B, false, ws.k3_grid, st);
+      out.launches += 2;
+    }
+    CK(cudaGetLastError());
+    batch = std::min(batch * 2, 64);
+  }
+  if (timings) CK(cudaEventRecord(ws.ev[3], st));
+  const Ctl& c = *ws.h_ctl;
+  out.rounds = c.round;
+  out.kept = rq.mode == SH_MODE_WITH_PREPROCESS ? c.kept : n;
+  out.bad = c.bad_index;
+  switch (c.status) {
+    case ST_DONE:
+      out.h = c.S_cur;
+      break;
+    case ST_SINGLE:
+      out.h = 1;
+      out.kept = rq.mode == SH_MODE_WITH_PREPROCESS ? n : n;
+      break;
+    case ST_COLLINEAR:
+      out.h = 2;
+      break;
+    case ST_NONFINITE:
+      out.code = SH_NON_FINITE_INPUT;
+      out.msg = "run: non-finite coordinate at index " + std::to_string(c.bad_index);
+      break;
+    case ST_INTERNAL:
+      out.code = SH_INTERNAL_ERROR;
+      out.msg = "run: refinement failed to terminate";
+      break;
+    case ST_OVERFLOW:
+      out.code = -1;  // caller regrows the segment tables
+      break;
+    default:
+      out.code = SH_INTERNAL_ERROR;
+      out.msg = "run: unexpected device status " + std::to_string(c.status);
+  }
+  (void)ph;
+  return out;
+}
+
+int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
+  if (!rq || !res) return SH_INVALID_ARGUMENT;
+  res->h = 0;
+  res->rounds = 0;
+  res->kept = 0;
+  res->bad_index = 0;
+  res->kernel_launches = 0;
+  res->err[0] = 0;
+  std::memset(&res->phases, 0, sizeof(res->phases));
+  const uint64_t n = rq->n;
+  if (n == 0) {
+    put_err(res->err, sizeof(res->err), "run: empty point set");
+    return SH_EMPTY_INPUT;  // hull.cpp:221
+  }
+  if (n >= 0xFFFFFFF0ull) {
+    put_err(res->err, sizeof(res->err), "run: input too large for 32-bit point ids");
+    return SH_INPUT_TOO_LARGE;
+  }
+  if (!rq->x || !rq->y) return SH_INVALID_ARGUMENT;
+  if (rq->mode != SH_MODE_WITH_PREPROCESS && rq->mode != SH_MODE_WITHOUT_PREPROCESS)
+    return SH_INVALID_ARGUMENT;
+  std::unique_ptr<Workspace> ws;
+  int prev_dev = 0;
+  cudaGetDevice(&prev_dev);
+  try {
+    CK(cudaSetDevice(rq->device));
+    ws = acquire(rq->device, n);
+    const bool timings = (rq->flags & SH_PHASE_TIMINGS) != 0;
+    cudaStream_t st = rq->stream ? (cudaStream_t)rq->stream : ws->stream;
+    RunOut o = run_pipeline(*ws, *rq, st, timings, &res->phases);
+    if (o.code == -1) {  // segment tables too small: regrow to n + 2 and rerun
+      const int dev = ws->device;
+      ws.reset();
+      ws = make_workspace(dev, std::max<uint64_t>(n, 1u << 12), n + 2);
+      o = run_pipeline(*ws, *rq, st, timings, &res->phases);
+      if (o.code == -1) {
+        o.code = SH_INTERNAL_ERROR;
+        o.msg = "run: segment table overflow";
+      }
+    }
+    res->rounds = o.rounds;
+    res->kept = o.kept;
+    res->bad_index = o.bad;
+    res->kernel_launches = o.launches;
+    res->h = o.h;
+    if (o.code != SH_OK) {
+      put_err(res->err, sizeof(res->err), o.msg);
+      release(std::move(ws));
+      cudaSetDevice(prev_dev);
+      return o.code;
+    }
+    const Ctl& c = *ws->h_ctl;
+    // vertices
+    if (o.h > res->cap && (res->x || res->y || res->idx)) {
+      put_err(res->err, sizeof(res->err), "output capacity too small");
+      release(std::move(ws));
+      cudaSetDevice(prev_dev);
+      return SH_CAP_TOO_SMALL;
+    }
+    if (c.status == ST_DONE) {
+      const uint32_t par = c.parity;
+      if (res->x) CK(cudaMemcpyAsync(res->x, ws->B.Tx[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
+      if (res->y) CK(cudaMemcpyAsync(res->y, ws->B.Ty[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
+      std::vector<uint32_t> ids;
+      if (res->idx) {
+        ids.resize(o.h);
+        CK(cudaMemcpyAsync(ids.data(), ws->B.Tid[par], 4 * o.h, cudaMemcpyDeviceToHost, st));
+      }
+      const uint64_t nst = std::min<uint64_t>({o.rounds, (uint64_t)STATS_CAP, res->stats ? res->stats_cap : 0});
+      if (nst) CK(cudaMemcpyAsync(ws->h_stats, ws->B.stats, sizeof(StatRec) * nst, cudaMemcpyDeviceToHost, st));
+      if (timings) CK(cudaEventRecord(ws->ev[4], st));
+      CK(cudaStreamSynchronize(st));
+      for (uint64_t i = 0; res->idx && i < o.h; ++i) res->idx[i] = ids[i];
+      for (uint64_t i = 0; i < nst; ++i) {
+        res->stats[i].iteration = i + 1;
+        res->stats[i].segments = ws->h_stats[i].segments;
+        res->stats[i].points_remaining = ws->h_stats[i].points_remaining;
+        res->stats[i].points_removed = ws->h_stats[i].points_removed;
+      }
+    } else {
+      // degenerate: {lo} or {lo, hi} (hull.cpp:234-248)
+      const int which[2] = {0, 2};
+      for (uint64_t i = 0; i < o.h; ++i) {
+        if (res->x) res->x[i] = c.ext_x[which[i]];
+        if (res->y) res->y[i] = c.ext_y[which[i]];
+        if (res->idx) res->idx[i] = c.ext_id[which[i]];
+      }
+      if (timings) CK(cudaEventRecord(ws->ev[4], st));
+      CK(cudaStreamSynchronize(st));
+    }
+    if (timings) {
+      float a = 0, b = 0, d = 0, t = 0;
+      if (c.status == ST_DONE) {
+        CK(cudaEventElapsedTime(&a, ws->ev[0], ws->ev[1]));
+        CK(cudaEventElapsedTime(&b, ws->ev[1], ws->ev[2]));
+        CK(cudaEventElapsedTime(&d, ws->ev[2], ws->ev[3]));
+      }
+      CK(cudaEventElapsedTime(&t, ws->ev[0], ws->ev[4]));
+      res->phases.pre_ms = a;
+      res->phases.split_ms = b;
+      res->phases.recurse_ms = d;
+      res->phases.total_ms = t;
+    }
+    release(std::move(ws));
+    cudaSetDevice(prev_dev);
+    return SH_OK;
+  } catch (const CudaFail& f) {
+    put_err(res->err, sizeof(res->err),
+            std::string("CUDA error: ") + cudaGetErrorString(f.err) + " at " + f.what);
+    cudaGetLastError();
+    if (ws) {
+      // a failed workspace is not returned to the pool
+      ws.reset();
+    }
+    cudaSetDevice(prev_dev);
+    return SH_CUDA_ERROR;
+  } catch (const std::bad_alloc&) {
+    put_err(res->err, sizeof(res->err), "host allocation failed");
+    cudaSetDevice(prev_dev);
+    return SH_CUDA_ERROR;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sh_b200_abi_version(void) { return SH_B200_ABI_VERSION; }
+
+int sh_b200_hull_ex(const sh_hull_request* req, sh_hull_result* res) { return hull_impl(req, res); }
+
+int sh_b200_hull(const double* x, const double* y, uint64_t n, int mode, uint32_t flags,
+                 int device, int64_t* out_idx, double* out_x, double* out_y, uint64_t cap,
+                 uint64_t* out_h, sh_round_stat* stats, uint64_t stats_cap,
+                 uint64_t* out_rounds, sh_phase_ms* phases, char* err, size_t errlen) {
+  sh_hull_request rq;
+  std::memset(&rq, 0, sizeof(rq));
+  rq.x = x;
+  rq.y = y;
+  rq.n = n;
+  rq.mode = mode;
+  rq.flags = flags;
+  rq.device = device;
+  sh_hull_result res;
+  std::memset(&res, 0, sizeof(res));
+  res.idx = out_idx;
+  res.x = out_x;
+  res.y = out_y;
+  res.cap = cap;
+  res.stats = stats;
+  res.stats_cap = stats_cap;
+  const int rc = hull_impl(&rq, &res);
+  if (out_h) *out_h = res.h;
+  if (out_rounds) *out_rounds = res.rounds;
+  if (phases) *phases = res.phases;
+  put_err(err, errlen, res.err);
+  return rc;
+}
+
+int sh_b200_gen_uniform(double* x, double* y, uint64_t first, uint64_t count, uint64_t seed,
+                        int device, void* stream) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) return SH_CUDA_ERROR;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, (uint64_t)sms * 16));
+  launch_gen_uniform(x, y, first, count, seed, grid, (cudaStream_t)stream);
+  const cudaError_t e = cudaGetLastError();
+  cudaSetDevice(prev);
+  return e == cudaSuccess ? SH_OK : SH_CUDA_ERROR;
+}
+
+int sh_b200_gen_disk(double* x, double* y, uint64_t n, uint64_t seed, int device, void* stream) {
+  if (n == 0) return SH_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  std::unique_ptr<Workspace> ws;
+  try {
+    CK(cudaSetDevice(device));
+    ws = acquire(device, n);
+    cudaStream_t st = stream ? (cudaStream_t)stream : ws->stream;
+    Ctl init;
+    std::memset(&init, 0, sizeof(init));
+    *ws->h_ctl = init;
+    CK(cudaMemcpyAsync(ws->B.ctl, ws->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    uint64_t accepted = 0, cand0 = 0;
+    const uint64_t max_batch = (uint64_t)(ws->tiles_cap - 64) * TILE;
+    while (accepted < n) {
+      const uint64_t need = n - accepted;
+      uint64_t batch = need + need / 4 + 4096;
+      batch = std::min<uint64_t>(batch, max_batch);
+      launch_gen_disk(x, y, n, seed, cand0, (uint32_t)batch, accepted, ws->B.ctl,
+                      ws->B.tile_status, ws->epoch, ws->k3_grid, st);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(ws->h_ctl, ws->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      accepted += ws->h_ctl->m_next;
+      cand0 += batch;
+    }
+    release(std::move(ws));
+    cudaSetDevice(prev);
+    return SH_OK;
+  } catch (const CudaFail&) {
+    cudaGetLastError();
+    cudaSetDevice(prev);
+    return SH_CUDA_ERROR;
+  }
+}
+
+int sh_b200_gen_circle_host(double* x, double* y, uint64_t n, uint64_t seed) {
+  uint64_t state = seed;
+  const double two_pi = 2.0 * 3.141592653589793;  // std::numbers::pi
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const double angle = two_pi * ((double)(z >> 11) * 0x1.0p-53);
+    x[i] = std::cos(angle);
+    y[i] = std::sin(angle);
+  }
+  return SH_OK;
+}
+
+int sh_b200_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
+                        uint64_t* hbm_bytes, char* name, size_t namelen) {
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, device) != cudaSuccess) {
+    cudaGetLastError();
+    return SH_CUDA_ERROR;
+  }
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  if (hbm_bytes) *hbm_bytes = p.totalGlobalMem;
+  if (name && namelen) std::snprintf(name, namelen, "%s", p.name);
+  return SH_OK;
+}
+
+void sh_b200_release_pool(void) {
+  std::lock_guard<std::mutex> lk(g_mutex);
+  g_pool.clear();
+}
+
+}  // extern "C"

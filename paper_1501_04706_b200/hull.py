@@ -1,0 +1,235 @@
+"""Host-side mirror of the reference's hull interface, backed by the sm_100a library.
+
+Mirrors /root/reference/proj/core/include/seghull/hull.hpp:35-95 and
+error.hpp:8-48 name for name so callers (and our parity tests) read like the
+reference's own tests (tests/test_hull.cpp):
+
+    result = hull.run(points, Mode.WithPreprocess, Backend.B200)
+    result.vertices      # CCW from the leftmost vertex (hull.hpp:53-59)
+    result.stats         # one SegmentStats per refinement round (hull.hpp:35-40)
+    result.phase_timings # PhaseTimings (hull.hpp:42-46), device time per phase
+
+Additions the reference does not have: ``result.indices`` (canonical input
+index of each vertex), ``result.kept`` (Mode-1 filter survivors) and the
+device-pointer / stream / ids options of :func:`run_arrays`.
+
+Every compute call goes through libseghull_b200.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+
+
+class Errc(enum.IntEnum):
+    """error.hpp:8-19"""
+    EmptyInput = 0
+    NonFiniteInput = 1
+    DegenerateInput = 2
+    InputTooLarge = 3
+    InternalError = 4
+    FileNotFound = 5
+    ParseError = 6
+    UnsupportedFormat = 7
+    IoError = 8
+    VerificationFailed = 9
+
+
+class Error(RuntimeError):
+    """error.hpp:39-48 -- single exception type; ``code()`` gives the Errc."""
+
+    def __init__(self, code: Errc, what: str):
+        super().__init__(what)
+        self._code = code
+
+    def code(self) -> Errc:
+        return self._code
+
+
+class CudaError(RuntimeError):
+    """The CUDA runtime failed (no device, out of memory, launch failure)."""
+
+
+class Mode(enum.IntEnum):
+    """hull.hpp:48-51"""
+    WithPreprocess = 1
+    WithoutPreprocess = 2
+
+
+class Backend(enum.IntEnum):
+    """primitives.hpp:14 plus the enumerator this library adds."""
+    Sequential = 0
+    Multicore = 1
+    B200 = 2
+
+
+@dataclass(frozen=True)
+class Point:
+    """geometry.hpp:8-13"""
+    x: float
+    y: float
+
+
+@dataclass
+class PointSet:
+    """dataio.hpp:14-30 -- structure of arrays."""
+    x: np.ndarray
+    y: np.ndarray
+
+    def __post_init__(self):
+        self.x = np.ascontiguousarray(self.x, dtype=np.float64)
+        self.y = np.ascontiguousarray(self.y, dtype=np.float64)
+        if self.x.shape != self.y.shape or self.x.ndim != 1:
+            raise ValueError("PointSet: x and y must be 1-D arrays of equal length")
+
+    @classmethod
+    def from_points(cls, pts: Sequence) -> "PointSet":
+        return cls(np.array([float(p[0]) for p in pts]), np.array([float(p[1]) for p in pts]))
+
+    def size(self) -> int:
+        return int(self.x.size)
+
+    def empty(self) -> bool:
+        return self.x.size == 0
+
+    def point(self, i: int) -> Point:
+        return Point(float(self.x[i]), float(self.y[i]))
+
+
+@dataclass(frozen=True)
+class SegmentStats:
+    """hull.hpp:35-40"""
+    iteration: int
+    segments: int
+    points_remaining: int
+    points_removed: int
+
+
+@dataclass(frozen=True)
+class PhaseTimings:
+    """hull.hpp:42-46 (device milliseconds from CUDA events); total_ms is ours."""
+    pre_ms: float = 0.0
+    split_ms: float = 0.0
+    recurse_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+@dataclass
+class HullResult:
+    """hull.hpp:53-59, plus canonical input indices of the vertices."""
+    x: np.ndarray
+    y: np.ndarray
+    indices: np.ndarray
+    stats: list = field(default_factory=list)
+    phase_timings: PhaseTimings = PhaseTimings()
+    kept: int = 0
+    rounds: int = 0
+    kernel_launches: int = 0
+
+    @property
+    def vertices(self) -> list:
+        return [Point(float(a), float(b)) for a, b in zip(self.x, self.y)]
+
+    def __len__(self) -> int:
+        return int(self.x.size)
+
+
+_ERRC_OF_STATUS = {1: Errc.EmptyInput, 2: Errc.NonFiniteInput, 3: Errc.DegenerateInput,
+                   4: Errc.InputTooLarge, 5: Errc.InternalError}
+
+
+def _raise(rc: int, msg: str):
+    if rc in _ERRC_OF_STATUS:
+        raise Error(_ERRC_OF_STATUS[rc], msg)
+    if rc == 101:
+        raise CudaError(msg or "CUDA error")
+    raise RuntimeError(f"sh_b200_hull_ex failed with status {rc}: {msg}")
+
+
+def _ptr_of(a):
+    """(device_pointer, is_device) for a numpy array or a CUDA torch tensor."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data, False
+    if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):
+        if not a.is_contiguous():
+            raise ValueError("tensor inputs must be contiguous")
+        return a.data_ptr(), bool(a.is_cuda)
+    raise TypeError(f"unsupported array type {type(a)!r}")
+
+
+def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int | None = None,
+               stream: int | None = None, timings: bool = False, stats: bool = True,
+               cap: int | None = None) -> HullResult:
+    """Hull of (x[i], y[i]).  x/y: float64 numpy arrays (host) or CUDA tensors
+    (device-resident, no H2D).  ``ids``: optional uint32 ids (same kind as x)
+    used for duplicate tie-breaks and returned as ``indices``."""
+    L = _lib.load()
+    if isinstance(x, np.ndarray):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        if ids is not None:
+            ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    else:
+        import torch
+        if x.dtype != torch.float64 or y.dtype != torch.float64:
+            raise TypeError("device inputs must be float64 tensors")
+        if ids is not None and ids.dtype not in (torch.int32, torch.uint32):
+            raise TypeError("device ids must be 32-bit integer tensors")
+    px, dx = _ptr_of(x)
+    py, dy = _ptr_of(y)
+    if dx != dy:
+        raise ValueError("x and y must both be host arrays or both device tensors")
+    n = int(x.shape[0])
+    if int(y.shape[0]) != n:
+        raise ValueError("x and y differ in length")
+    if device is None:
+        device = int(x.device.index) if dx else 0
+    req = _lib.sh_hull_request()
+    req.x = px
+    req.y = py
+    req.n = n
+    req.ids = _ptr_of(ids)[0] if ids is not None else None
+    req.mode = int(mode)
+    req.flags = (_lib.SH_DEVICE_PTRS if dx else _lib.SH_HOST_PTRS) | (
+        _lib.SH_PHASE_TIMINGS if timings else 0)
+    req.device = int(device)
+    req.stream = stream
+    capacity = max(int(cap if cap is not None else max(n, 2)), 2)
+    ox = np.empty(capacity, np.float64)
+    oy = np.empty(capacity, np.float64)
+    oi = np.empty(capacity, np.int64)
+    stats_cap = 1 << 16 if stats else 0
+    st = (_lib.sh_round_stat * max(stats_cap, 1))()
+    res = _lib.sh_hull_result()
+    res.idx = oi.ctypes.data
+    res.x = ox.ctypes.data
+    res.y = oy.ctypes.data
+    res.cap = capacity
+    res.stats = ctypes.addressof(st) if stats else None
+    res.stats_cap = stats_cap
+    rc = L.sh_b200_hull_ex(ctypes.byref(req), ctypes.byref(res))
+    if rc != 0:
+        _raise(rc, res.err.decode(errors="replace"))
+    h = int(res.h)
+    nst = min(int(res.rounds), stats_cap)
+    sts = [SegmentStats(int(st[i].iteration), int(st[i].segments), int(st[i].points_remaining),
+                        int(st[i].points_removed)) for i in range(nst)]
+    ph = PhaseTimings(res.phases.pre_ms, res.phases.split_ms, res.phases.recurse_ms,
+                      res.phases.total_ms)
+    return HullResult(ox[:h].copy(), oy[:h].copy(), oi[:h].copy(), sts, ph, int(res.kept),
+                      int(res.rounds), int(res.kernel_launches))
+
+
+def run(points: PointSet, mode: Mode = Mode.WithPreprocess,
+        backend: Backend = Backend.B200) -> HullResult:
+    """seghull::hull::run (hull.hpp:95) on the B200 backend."""
+    if backend != Backend.B200:
+        raise ValueError("this package implements Backend.B200 only; the Sequential/Multicore "
+                         "backends are the reference's own CPU code")
+    return run_arrays(points.x, points.y, mode)
