@@ -57,7 +57,9 @@ enum sh_flags {
   SH_HOST_PTRS = 0u,      /* x, y (and idx) are host memory: H2D inside the call   */
   SH_DEVICE_PTRS = 1u,    /* x, y (and idx) are device memory on `device`          */
   SH_PHASE_TIMINGS = 2u,  /* record CUDA events per phase into sh_phase_ms         */
-  SH_NO_STATS = 4u        /* skip the per-round stats read-back                    */
+  SH_NO_STATS = 4u,       /* skip the per-round stats read-back                    */
+  SH_OUT_DEVICE = 8u      /* out_idx/out_x/out_y are device memory on `device`:      */
+                          /* the vertices never leave HBM (shard hulls -> gather)    */
 };
 
 /* hull.hpp:35-40 SegmentStats */
@@ -75,6 +77,17 @@ typedef struct {
   double recurse_ms;  /* remaining rounds until only hull vertices remain         */
   double total_ms;    /* whole call on the device, H2D/D2H included when HOST_PTRS */
 } sh_phase_ms;
+
+/* Per-kernel device times of one call (CUDA events on the call's stream;
+ * filled with SH_PHASE_TIMINGS).  Used for the roofline fractions. */
+typedef struct {
+  double h2d_ms;         /* input host->device copy (HOST_PTRS only)            */
+  double extremes_ms;    /* K1: extremes + finite check                         */
+  double filter_ms;      /* K2: quad filter + chain classes + round-0 farthest  */
+  double first_round_ms; /* K3<first>: round 1 straight from the input          */
+  double rounds_ms;      /* K4/K3 rounds >= 2, including the status polls       */
+  double d2h_ms;         /* result read-back                                    */
+} sh_kernel_ms;
 
 /*
  * Convex hull of (x[i], y[i]), i < n.  Equivalent of
@@ -117,6 +130,7 @@ typedef struct {
   uint64_t kept;        /* points surviving the Mode-1 filter (n in Mode 2)      */
   uint64_t bad_index;   /* first non-finite index when SH_NON_FINITE_INPUT       */
   sh_phase_ms phases;
+  sh_kernel_ms kernels;
   uint32_t kernel_launches; /* kernels this call launched (evidence of GPU work) */
   char err[256];
 } sh_hull_result;

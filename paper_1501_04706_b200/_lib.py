@@ -28,6 +28,12 @@ class sh_phase_ms(ctypes.Structure):
                 ("recurse_ms", ctypes.c_double), ("total_ms", ctypes.c_double)]
 
 
+class sh_kernel_ms(ctypes.Structure):
+    _fields_ = [("h2d_ms", ctypes.c_double), ("extremes_ms", ctypes.c_double),
+                ("filter_ms", ctypes.c_double), ("first_round_ms", ctypes.c_double),
+                ("rounds_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double)]
+
+
 class sh_hull_request(ctypes.Structure):
     _fields_ = [("x", _vp), ("y", _vp), ("n", _u64), ("ids", _vp), ("mode", ctypes.c_int),
                 ("flags", _u32), ("device", ctypes.c_int), ("stream", _vp)]
@@ -36,7 +42,8 @@ class sh_hull_request(ctypes.Structure):
 class sh_hull_result(ctypes.Structure):
     _fields_ = [("idx", _vp), ("x", _vp), ("y", _vp), ("cap", _u64), ("h", _u64),
                 ("stats", _vp), ("stats_cap", _u64), ("rounds", _u64), ("kept", _u64),
-                ("bad_index", _u64), ("phases", sh_phase_ms), ("kernel_launches", _u32),
+                ("bad_index", _u64), ("phases", sh_phase_ms), ("kernels", sh_kernel_ms),
+                ("kernel_launches", _u32),
                 ("err", ctypes.c_char * 256)]
 
 
@@ -49,6 +56,7 @@ SH_HOST_PTRS = 0
 SH_DEVICE_PTRS = 1
 SH_PHASE_TIMINGS = 2
 SH_NO_STATS = 4
+SH_OUT_DEVICE = 8
 
 _lib = None
 

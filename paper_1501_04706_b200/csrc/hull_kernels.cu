@@ -1019,6 +1019,20 @@ __global__ void __launch_bounds__(TPB) k_gen_disk(double* x, double* y, unsigned
 }
 
 // ===========================================================================
+// K5: emit the hull (segment heads in table order) into caller device memory
+// ===========================================================================
+
+__global__ void k5_emit(const double* __restrict__ Tx, const double* __restrict__ Ty,
+                        const uint32_t* __restrict__ Tid, uint32_t h, double* ox, double* oy,
+                        long long* oidx) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x) {
+    if (ox) ox[i] = Tx[i];
+    if (oy) oy[i] = Ty[i];
+    if (oidx) oidx[i] = (long long)Tid[i];
+  }
+}
+
+// ===========================================================================
 // host-side launch wrappers
 // ===========================================================================
 
@@ -1055,6 +1069,12 @@ void launch_k3(const Bufs& B, bool first, int grid, cudaStream_t s) {
 }
 
 void launch_k4(const Bufs& B, int grid, cudaStream_t s) { k4_table<<<grid, TPB, 0, s>>>(B); }
+
+void launch_k5(const double* Tx, const double* Ty, const uint32_t* Tid, uint32_t h, double* ox,
+               double* oy, long long* oidx, cudaStream_t s) {
+  const int grid = (int)((h + 255) / 256 < 1024 ? (h + 255) / 256 : 1024);
+  k5_emit<<<grid < 1 ? 1 : grid, 256, 0, s>>>(Tx, Ty, Tid, h, ox, oy, oidx);
+}
 
 void launch_gen_uniform(double* x, double* y, unsigned long long first, unsigned long long count,
                         unsigned long long seed, int grid, cudaStream_t s) {

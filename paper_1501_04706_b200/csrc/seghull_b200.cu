@@ -28,6 +28,8 @@ void launch_k1(const Bufs& B, int grid, cudaStream_t s);
 void launch_k2(const Bufs& B, bool filter, int grid, int reverse, cudaStream_t s);
 void launch_k3(const Bufs& B, bool first, int grid, cudaStream_t s);
 void launch_k4(const Bufs& B, int grid, cudaStream_t s);
+void launch_k5(const double* Tx, const double* Ty, const uint32_t* Tid, uint32_t h, double* ox,
+               double* oy, long long* oidx, cudaStream_t s);
 void launch_gen_uniform(double* x, double* y, unsigned long long first, unsigned long long count,
                         unsigned long long seed, int grid, cudaStream_t s);
 void launch_gen_disk(double* x, double* y, unsigned long long n, unsigned long long seed,
@@ -71,7 +73,7 @@ struct Workspace {
   uint32_t* epoch = nullptr;
   Ctl* h_ctl = nullptr;        // pinned
   StatRec* h_stats = nullptr;  // pinned
-  cudaEvent_t ev[5] = {};
+  cudaEvent_t ev[8] = {};
   size_t tiles_cap = 0;
   int k1_grid = 0, k2_grid = 0, k3_grid = 0, k4_grid = 0;
 
@@ -271,7 +273,9 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, cudaStream_t st, b
     B.in_x = sx;
     B.in_y = sy;
     B.in_id = rq.ids ? sid : nullptr;
+    if (timings) CK(cudaEventRecord(ws.ev[1], st));
   } else {
+    if (timings) CK(cudaEventRecord(ws.ev[1], st));
     B.in_x = rq.x;
     B.in_y = rq.y;
     B.in_id = rq.ids;
@@ -289,11 +293,12 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, cudaStream_t st, b
 
   const int g1 = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + TPB - 1) / TPB, ws.k1_grid));
   launch_k1(B, g1, st);
+  if (timings) CK(cudaEventRecord(ws.ev[2], st));
   launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, g1, /*reverse=*/1, st);
-  if (timings) CK(cudaEventRecord(ws.ev[1], st));
+  if (timings) CK(cudaEventRecord(ws.ev[3], st));
   launch_k3(B, true, ws.k3_grid, st);
   out.launches = 3;
-  if (timings) CK(cudaEventRecord(ws.ev[2], st));
+  if (timings) CK(cudaEventRecord(ws.ev[4], st));
   CK(cudaGetLastError());
 
   // rounds >= 2 in growing batches; each kernel exits at once when the
@@ -311,7 +316,7 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, cudaStream_t st, b
     CK(cudaGetLastError());
     batch = std::min(batch * 2, 64);
   }
-  if (timings) CK(cudaEventRecord(ws.ev[3], st));
+  if (timings) CK(cudaEventRecord(ws.ev[5], st));
   const Ctl& c = *ws.h_ctl;
   out.rounds = c.round;
   out.kept = rq.mode == SH_MODE_WITH_PREPROCESS ? c.kept : n;
@@ -390,6 +395,7 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
     res->kept = o.kept;
     res->bad_index = o.bad;
     res->kernel_launches = o.launches;
+    std::memset(&res->kernels, 0, sizeof(res->kernels));
     res->h = o.h;
     if (o.code != SH_OK) {
       put_err(res->err, sizeof(res->err), o.msg);
@@ -405,20 +411,31 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
       cudaSetDevice(prev_dev);
       return SH_CAP_TOO_SMALL;
     }
+    const bool out_dev = (rq->flags & SH_OUT_DEVICE) != 0;
     if (c.status == ST_DONE) {
       const uint32_t par = c.parity;
-      if (res->x) CK(cudaMemcpyAsync(res->x, ws->B.Tx[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
-      if (res->y) CK(cudaMemcpyAsync(res->y, ws->B.Ty[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
-      std::vector<uint32_t> ids;
-      if (res->idx) {
-        ids.resize(o.h);
-        CK(cudaMemcpyAsync(ids.data(), ws->B.Tid[par], 4 * o.h, cudaMemcpyDeviceToHost, st));
-      }
       const uint64_t nst = std::min<uint64_t>({o.rounds, (uint64_t)STATS_CAP, res->stats ? res->stats_cap : 0});
+      std::vector<uint32_t> ids;
+      if (out_dev) {
+        // vertices stay in HBM: one emit kernel (u32 ids -> i64) on the call's stream
+        if (o.h && (res->x || res->y || res->idx)) {
+          launch_k5(ws->B.Tx[par], ws->B.Ty[par], ws->B.Tid[par], (uint32_t)o.h, res->x, res->y,
+                    (long long*)res->idx, st);
+          CK(cudaGetLastError());
+          res->kernel_launches += 1;
+        }
+      } else {
+        if (res->x) CK(cudaMemcpyAsync(res->x, ws->B.Tx[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
+        if (res->y) CK(cudaMemcpyAsync(res->y, ws->B.Ty[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
+        if (res->idx) {
+          ids.resize(o.h);
+          CK(cudaMemcpyAsync(ids.data(), ws->B.Tid[par], 4 * o.h, cudaMemcpyDeviceToHost, st));
+        }
+      }
       if (nst) CK(cudaMemcpyAsync(ws->h_stats, ws->B.stats, sizeof(StatRec) * nst, cudaMemcpyDeviceToHost, st));
-      if (timings) CK(cudaEventRecord(ws->ev[4], st));
+      if (timings) CK(cudaEventRecord(ws->ev[6], st));
       CK(cudaStreamSynchronize(st));
-      for (uint64_t i = 0; res->idx && i < o.h; ++i) res->idx[i] = ids[i];
+      for (uint64_t i = 0; !out_dev && res->idx && i < o.h; ++i) res->idx[i] = ids[i];
       for (uint64_t i = 0; i < nst; ++i) {
         res->stats[i].iteration = i + 1;
         res->stats[i].segments = ws->h_stats[i].segments;
@@ -428,26 +445,43 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
     } else {
       // degenerate: {lo} or {lo, hi} (hull.cpp:234-248)
       const int which[2] = {0, 2};
+      double vx[2] = {0, 0}, vy[2] = {0, 0};
+      int64_t vi[2] = {0, 0};
       for (uint64_t i = 0; i < o.h; ++i) {
-        if (res->x) res->x[i] = c.ext_x[which[i]];
-        if (res->y) res->y[i] = c.ext_y[which[i]];
-        if (res->idx) res->idx[i] = c.ext_id[which[i]];
+        vx[i] = c.ext_x[which[i]];
+        vy[i] = c.ext_y[which[i]];
+        vi[i] = c.ext_id[which[i]];
       }
-      if (timings) CK(cudaEventRecord(ws->ev[4], st));
+      if (out_dev) {
+        if (res->x) CK(cudaMemcpyAsync(res->x, vx, 8 * o.h, cudaMemcpyHostToDevice, st));
+        if (res->y) CK(cudaMemcpyAsync(res->y, vy, 8 * o.h, cudaMemcpyHostToDevice, st));
+        if (res->idx) CK(cudaMemcpyAsync(res->idx, vi, 8 * o.h, cudaMemcpyHostToDevice, st));
+      } else {
+        for (uint64_t i = 0; i < o.h; ++i) {
+          if (res->x) res->x[i] = vx[i];
+          if (res->y) res->y[i] = vy[i];
+          if (res->idx) res->idx[i] = vi[i];
+        }
+      }
+      if (timings) CK(cudaEventRecord(ws->ev[6], st));
       CK(cudaStreamSynchronize(st));
     }
     if (timings) {
-      float a = 0, b = 0, d = 0, t = 0;
-      if (c.status == ST_DONE) {
-        CK(cudaEventElapsedTime(&a, ws->ev[0], ws->ev[1]));
-        CK(cudaEventElapsedTime(&b, ws->ev[1], ws->ev[2]));
-        CK(cudaEventElapsedTime(&d, ws->ev[2], ws->ev[3]));
-      }
-      CK(cudaEventElapsedTime(&t, ws->ev[0], ws->ev[4]));
-      res->phases.pre_ms = a;
-      res->phases.split_ms = b;
-      res->phases.recurse_ms = d;
-      res->phases.total_ms = t;
+      auto el = [&](int i, int j) {
+        float v = 0.f;
+        CK(cudaEventElapsedTime(&v, ws->ev[i], ws->ev[j]));
+        return (double)v;
+      };
+      res->kernels.h2d_ms = el(0, 1);
+      res->kernels.extremes_ms = el(1, 2);
+      res->kernels.filter_ms = el(2, 3);
+      res->kernels.first_round_ms = el(3, 4);
+      res->kernels.rounds_ms = el(4, 5);
+      res->kernels.d2h_ms = el(5, 6);
+      res->phases.pre_ms = el(1, 3);
+      res->phases.split_ms = el(3, 4);
+      res->phases.recurse_ms = el(4, 5);
+      res->phases.total_ms = el(0, 6);
     }
     release(std::move(ws));
     cudaSetDevice(prev_dev);

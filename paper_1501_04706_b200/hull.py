@@ -131,6 +131,7 @@ class HullResult:
     kept: int = 0
     rounds: int = 0
     kernel_launches: int = 0
+    kernels: object = None
 
     @property
     def vertices(self) -> list:
@@ -163,13 +164,18 @@ def _ptr_of(a):
     raise TypeError(f"unsupported array type {type(a)!r}")
 
 
-def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int | None = None,
-               stream: int | None = None, timings: bool = False, stats: bool = True,
-               cap: int | None = None) -> HullResult:
-    """Hull of (x[i], y[i]).  x/y: float64 numpy arrays (host) or CUDA tensors
-    (device-resident, no H2D).  ``ids``: optional uint32 ids (same kind as x)
-    used for duplicate tie-breaks and returned as ``indices``."""
-    L = _lib.load()
+@dataclass(frozen=True)
+class KernelTimings:
+    """Per-kernel device milliseconds of one call (sh_kernel_ms)."""
+    h2d_ms: float = 0.0
+    extremes_ms: float = 0.0
+    filter_ms: float = 0.0
+    first_round_ms: float = 0.0
+    rounds_ms: float = 0.0
+    d2h_ms: float = 0.0
+
+
+def _prepare(x, y, ids):
     if isinstance(x, np.ndarray):
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.ascontiguousarray(y, dtype=np.float64)
@@ -178,9 +184,9 @@ def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int |
     else:
         import torch
         if x.dtype != torch.float64 or y.dtype != torch.float64:
-            raise TypeError("device inputs must be float64 tensors")
+            raise TypeError("tensor inputs must be float64")
         if ids is not None and ids.dtype not in (torch.int32, torch.uint32):
-            raise TypeError("device ids must be 32-bit integer tensors")
+            raise TypeError("tensor ids must be 32-bit integers")
     px, dx = _ptr_of(x)
     py, dy = _ptr_of(y)
     if dx != dy:
@@ -188,42 +194,108 @@ def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int |
     n = int(x.shape[0])
     if int(y.shape[0]) != n:
         raise ValueError("x and y differ in length")
-    if device is None:
-        device = int(x.device.index) if dx else 0
+    return x, y, ids, px, py, dx, n
+
+
+def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, stats_cap):
+    L = _lib.load()
     req = _lib.sh_hull_request()
     req.x = px
     req.y = py
     req.n = n
-    req.ids = _ptr_of(ids)[0] if ids is not None else None
+    req.ids = pids
     req.mode = int(mode)
-    req.flags = (_lib.SH_DEVICE_PTRS if dx else _lib.SH_HOST_PTRS) | (
-        _lib.SH_PHASE_TIMINGS if timings else 0)
+    req.flags = flags
     req.device = int(device)
     req.stream = stream
-    capacity = max(int(cap if cap is not None else max(n, 2)), 2)
-    ox = np.empty(capacity, np.float64)
-    oy = np.empty(capacity, np.float64)
-    oi = np.empty(capacity, np.int64)
-    stats_cap = 1 << 16 if stats else 0
     st = (_lib.sh_round_stat * max(stats_cap, 1))()
     res = _lib.sh_hull_result()
-    res.idx = oi.ctypes.data
-    res.x = ox.ctypes.data
-    res.y = oy.ctypes.data
+    res.idx = oi
+    res.x = ox
+    res.y = oy
     res.cap = capacity
-    res.stats = ctypes.addressof(st) if stats else None
+    res.stats = ctypes.addressof(st) if stats_cap else None
     res.stats_cap = stats_cap
     rc = L.sh_b200_hull_ex(ctypes.byref(req), ctypes.byref(res))
     if rc != 0:
         _raise(rc, res.err.decode(errors="replace"))
-    h = int(res.h)
     nst = min(int(res.rounds), stats_cap)
     sts = [SegmentStats(int(st[i].iteration), int(st[i].segments), int(st[i].points_remaining),
                         int(st[i].points_removed)) for i in range(nst)]
     ph = PhaseTimings(res.phases.pre_ms, res.phases.split_ms, res.phases.recurse_ms,
                       res.phases.total_ms)
-    return HullResult(ox[:h].copy(), oy[:h].copy(), oi[:h].copy(), sts, ph, int(res.kept),
-                      int(res.rounds), int(res.kernel_launches))
+    k = res.kernels
+    kt = KernelTimings(k.h2d_ms, k.extremes_ms, k.filter_ms, k.first_round_ms, k.rounds_ms,
+                       k.d2h_ms)
+    return res, sts, ph, kt
+
+
+def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int | None = None,
+               stream: int | None = None, timings: bool = False, stats: bool = True,
+               cap: int | None = None) -> HullResult:
+    """Hull of (x[i], y[i]).  x/y: float64 numpy arrays or CPU tensors (host; the
+    H2D copy happens inside the call) or CUDA tensors (device-resident, no H2D).
+    ``ids``: optional uint32 ids (same kind as x) used for duplicate tie-breaks
+    and returned as ``indices``.  The result is returned in host memory."""
+    x, y, ids, px, py, dx, n = _prepare(x, y, ids)
+    if device is None:
+        device = int(x.device.index) if dx else 0
+    capacity = max(int(cap if cap is not None else max(n, 2)), 2)
+    ox = np.empty(capacity, np.float64)
+    oy = np.empty(capacity, np.float64)
+    oi = np.empty(capacity, np.int64)
+    flags = (_lib.SH_DEVICE_PTRS if dx else _lib.SH_HOST_PTRS) | (
+        _lib.SH_PHASE_TIMINGS if timings else 0)
+    res, sts, ph, kt = _call(px, py, n, _ptr_of(ids)[0] if ids is not None else None, mode,
+                             flags, device, stream, ox.ctypes.data, oy.ctypes.data,
+                             oi.ctypes.data, capacity, (1 << 16) if stats else 0)
+    h = int(res.h)
+    r = HullResult(ox[:h].copy(), oy[:h].copy(), oi[:h].copy(), sts, ph, int(res.kept),
+                   int(res.rounds), int(res.kernel_launches))
+    r.kernels = kt
+    return r
+
+
+@dataclass
+class DeviceHull:
+    """A hull whose vertices stay in HBM (SH_OUT_DEVICE): torch CUDA tensors."""
+    x: object
+    y: object
+    indices: object
+    h: int
+    stats: list
+    phase_timings: PhaseTimings
+    kernels: KernelTimings
+    kept: int
+    rounds: int
+    kernel_launches: int
+
+
+def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int | None = None,
+               timings: bool = False, stats: bool = True, out=None) -> DeviceHull:
+    """Hull of device-resident float64 CUDA tensors; the vertices are written to
+    device tensors (``out`` = (x, y, idx) buffers of equal capacity, else
+    allocated at len(x)).  Only h, the stats and timings cross to the host."""
+    import torch
+    x, y, ids, px, py, dx, n = _prepare(x, y, ids)
+    if not dx:
+        raise ValueError("run_device needs CUDA tensors")
+    device = int(x.device.index)
+    if out is None:
+        cap = max(n, 2)
+        out = (torch.empty(cap, dtype=torch.float64, device=x.device),
+               torch.empty(cap, dtype=torch.float64, device=x.device),
+               torch.empty(cap, dtype=torch.int64, device=x.device))
+    ox, oy, oi = out
+    if stream is None:
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+    flags = _lib.SH_DEVICE_PTRS | _lib.SH_OUT_DEVICE | (_lib.SH_PHASE_TIMINGS if timings else 0)
+    res, sts, ph, kt = _call(px, py, n, ids.data_ptr() if ids is not None else None, mode, flags,
+                             device, stream, ox.data_ptr(), oy.data_ptr(), oi.data_ptr(),
+                             int(ox.shape[0]), (1 << 16) if stats else 0)
+    h = int(res.h)
+    return DeviceHull(ox[:h], oy[:h], oi[:h], h, sts, ph, kt, int(res.kept), int(res.rounds),
+                      int(res.kernel_launches))
 
 
 def run(points: PointSet, mode: Mode = Mode.WithPreprocess,
