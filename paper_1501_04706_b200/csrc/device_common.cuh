@@ -140,27 +140,28 @@ SH_DEV uint32_t lanemask_lt() {
 }
 
 // ---------------------------------------------------------------------------
-// Global farthest-point slot: 64-bit atomicMax on the distance bits (positive
-// doubles order like their bit patterns) as a contention filter, then a CAS
-// loop on the winner's position with the full comparator.  The current
-// winner's distance is recomputed from its stored coordinates against the
-// same edge, so slots hold only (dbits, position).
-//   src_x/src_y/src_id : arrays the position indexes (src_id NULL => id = pos)
-// Callers must have made the candidate's row visible (__threadfence) first.
+// Farthest-point slot {dbits, win}: a 64-bit atomicMax on the distance bits
+// (positive doubles order like their bit patterns) filters contention, then a
+// CAS loop on the winner's position applies the full comparator.  The
+// incumbent's distance is recomputed from its stored coordinates against the
+// slot's edge -- every contender of a slot belongs to the same new segment,
+// so the caller's own edge IS the slot's edge and the recomputed value is
+// bit-identical to the one the incumbent offered.
+//   LD : functor (pos) -> (x, y, id) reading the array the positions index
+// Callers must have made the candidate's own row visible (__threadfence)
+// before offering.  Works on global and on shared slots (generic atomics).
+template <class LD>
 SH_DEV void slot_offer(unsigned long long* dbits, uint32_t* win, const Cand& c, bool lower,
-                       const Edge& e, const double* src_x, const double* src_y,
-                       const uint32_t* src_id) {
+                       const Edge& e, const LD& ld) {
   const unsigned long long mine = (unsigned long long)__double_as_longlong(c.d);
-  if (mine < ld_relaxed_u64(dbits)) return;
+  if (mine < *(volatile unsigned long long*)dbits) return;
   const unsigned long long old = atomicMax(dbits, mine);
   if (mine < old) return;
-  uint32_t cur = ld_acquire_u32(win);
+  uint32_t cur = *(volatile uint32_t*)win;
   while (true) {
     if (cur != NONE) {
       Cand o;
-      o.x = __ldcg(src_x + cur);
-      o.y = __ldcg(src_y + cur);
-      o.id = src_id ? __ldcg(src_id + cur) : cur;
+      ld(cur, o.x, o.y, o.id);
       o.d = outward_e(e, o.x, o.y);
       o.pos = cur;
       if (!cand_better(c, o, lower)) return;
@@ -168,8 +169,62 @@ SH_DEV void slot_offer(unsigned long long* dbits, uint32_t* win, const Cand& c, 
     const uint32_t prev = atomicCAS(win, cur, c.pos);
     if (prev == cur) return;
     cur = prev;
+  }
+}
+
+// (x, y, id) of a position in SoA input arrays (ids null => id == position)
+struct LoadSoA {
+  const double* x;
+  const double* y;
+  const uint32_t* id;
+  SH_DEV void operator()(uint32_t p, double& ox, double& oy, uint32_t& oid) const {
+    ox = __ldcg(x + p);
+    oy = __ldcg(y + p);
+    oid = id ? __ldcg(id + p) : p;
+  }
+};
+
+// (x, y, id) of a position in a live set
+struct LoadLive {
+  const double2* xy;
+  const uint2* is;
+  SH_DEV void operator()(uint32_t p, double& ox, double& oy, uint32_t& oid) const {
+    const double2 v = __ldcg(xy + p);
+    ox = v.x;
+    oy = v.y;
+    oid = __ldcg(&is[p].x);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Grid barrier for a cooperative launch (all CTAs co-resident).  The
+// generation word is read before arriving, so a fast CTA re-entering the
+// next barrier cannot be confused with the current one.
+SH_DEV void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+SH_DEV void grid_barrier(uint32_t* count, uint32_t* gen, uint32_t nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t g;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      *(volatile uint32_t*)count = 0u;
+      __threadfence();
+      st_release_u32(gen, g + 1);
+    } else {
+      uint32_t v;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gen) : "memory");
+        if (v != g) break;
+        __nanosleep(20);
+      }
+    }
     __threadfence();
   }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------

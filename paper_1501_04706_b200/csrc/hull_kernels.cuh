@@ -1,27 +1,42 @@
 // hull_kernels.cuh -- data layout shared by the host orchestration and the
 // sm_100a kernels of the segment-based QuickHull.
 //
-// HBM layout (SoA everywhere, per workspace):
-//   input        x[n], y[n] f64 (+ optional ids[n] u32)
-//   chain bits   lo[ceil(n/32)], up[ceil(n/32)] u32: K2's per-point class
-//   live set L   ping-pong {x f64, y f64, id u32, seg u32}[n]   24 B/point
-//   segment tbl  ping-pong heads {x f64, y f64, id u32}[S]        20 B/segment
-//   farthest     ping-pong slots {dbits u64, win u32}[S]         12 B/segment
-//   route tbl    Route[S] 64 B: the (A, C, B) triangle of each old segment
-//   tile status  u64[tiles] for the decoupled look-back scans
+// HBM layout (per workspace):
+//   input        x[n], y[n] f64 SoA (caller's, or the H2D staging copy)
+//                (+ optional ids[n] u32 -- global ids of a shard-merge input)
+//   chain bits   uint4[ceil(n/64)]: K2's per-point class for one 64-point
+//                chunk {lower even, lower odd, upper even, upper odd}; bit l of
+//                word "even" is point 64c+2l, of "odd" point 64c+2l+1
+//   live set     ping-pong {xy double2, (id, seg) uint2}[n]      24 B/point
+//   head table   ping-pong {x f64, y f64, id u32}[S]              20 B/segment
+//   farthest     3-way rotating slots {dbits u64, win u32}[S]     12 B/segment
+//   route table  Route[S] 64 B (large tables only; small ones live in smem)
+//
+// Round numbering follows hull.cpp:264-282: round r >= 1 splits the
+// segments of round r-1 at their farthest points, routes every member to
+// the A->C or C->B edge and drops the interior ones.  "Round 0" is K2 (the
+// first split + the round-1 farthest points).
+//   round r reads  heads Tab[(r-1)&1], farthest slots Slot[(r-1)%3],
+//                  live set Live[(r-1)&1] (round 1: the input)
+//   round r writes heads Tab[r&1], slots Slot[r%3] (next round's farthest
+//                  points), live set Live[r&1], survivor count out_cnt[r%3]
+//   round r clears Slot[(r+1)%3] and out_cnt[(r+1)%3] for round r+1
+// so no buffer is ever cleared while another CTA may still read it.
 #pragma once
 
 #include <cstdint>
 
 namespace shb {
 
-constexpr int TPB = 256;           // threads per block of the streaming kernels
+constexpr int TPB = 256;             // K1 / K2 / K3 (streaming kernels)
 constexpr int WARPS = TPB / 32;
-constexpr int ITEMS = 8;           // points per thread per tile
-constexpr int TILE = TPB * ITEMS;  // 2048 points per tile
-constexpr int NSLOT = 1024;        // per-block shared-memory farthest slots
-constexpr uint32_t SMALL_S = 4096; // segment tables up to this size are built by one block
+constexpr int RTPB = 512;            // persistent round kernel
+constexpr int SMALL_S = 1024;        // tables up to this size are rebuilt per CTA in smem
+constexpr int NSLOT = 2 * SMALL_S;   // next-round segments of a small table
+constexpr uint32_t TAIL_M = 4096;    // live sets up to this size finish in one CTA
 constexpr int STATS_CAP = 1 << 16;
+constexpr int STATS_EAGER = 64;      // stats read back together with the control block
+constexpr int MAX_ROUND_BLOCKS = 1024;
 
 enum Status : uint32_t {
   ST_RUNNING = 0,
@@ -43,11 +58,12 @@ struct K1Partial {
   unsigned long long bad;
 };
 
-// 64-byte route entry of an old segment s: head A, next head B, farthest C.
+// 64-byte route entry of an old segment s: head A, farthest point C, next
+// head B (hull.cpp:186-201 restated per segment).
 struct __align__(16) Route {
   double ax, ay, cx, cy, bx, by;
   uint32_t cid;    // id of C (it becomes a head and leaves the member set)
-  uint32_t ns;     // index of s in the next segment table
+  uint32_t ns;     // index of s in the next head table
   uint32_t flags;  // RT_SPLIT | RT_LOWER
   uint32_t pad;
 };
@@ -57,31 +73,30 @@ struct StatRec {
   uint32_t segments, points_remaining, points_removed, pad;
 };
 
-// Device-resident control block: all round bookkeeping lives here so the
-// host never has to read anything between rounds.
+// Device-resident control block.  The host writes it once per call and
+// reads it once at the end; all round bookkeeping stays on the device.
 struct Ctl {
   uint32_t status;
-  uint32_t parity;      // which ping-pong half is current
   uint32_t round;       // refinement rounds completed
-  uint32_t table_ready; // route table for the next round already built
+  uint32_t S_cur;       // segments after `round`
+  uint32_t Slo_cur;     // of which lower-chain segments
+  uint32_t m_cur;       // live members after `round`
+  uint32_t n;
   unsigned long long bad_index;
   // extremes: left, bottom, right, top (K1)
   double ext_x[4], ext_y[4];
   uint32_t ext_id[4], ext_pos[4];
   int distinct, nedges;
   double edges[4][4];   // hoisted (ax, ay, ex, ey) of the quadrilateral edges
-  // K2
   unsigned long long kept;
   uint32_t noncollinear;
-  // rounds
-  uint32_t S_cur, Slo_cur, m_cur;
-  uint32_t S_next, Slo_next, m_next;
-  // tickets
-  uint32_t ticket, tile_ctr;
-  uint32_t n;
-  uint32_t s_cap;
+  uint32_t ticket;      // last-CTA ticket of K1 / K2 / K3
+  uint32_t out_cnt[3];  // survivors of round r accumulate in out_cnt[r % 3]
+  uint32_t bar_count;   // grid barrier of the round kernel
+  uint32_t bar_gen;
   uint32_t mode;
-  uint32_t pad0;
+  uint32_t tile_ctr;    // generator scratch
+  uint32_t m_next;      // generator scratch
 };
 
 struct Bufs {
@@ -93,29 +108,24 @@ struct Bufs {
   uint32_t s_cap;
   // control
   Ctl* ctl;
-  uint32_t* epoch;        // persistent launch-epoch counter (never reset)
+  uint32_t* epoch;        // launch-epoch counter of the generator's look-back scan
   K1Partial* k1part;
   StatRec* stats;
   unsigned long long* tile_status;
+  uint32_t* blk_cnt;      // [2 * MAX_ROUND_BLOCKS] per-CTA counts of a large table scan
   // classification bits
-  uint32_t* bits_lo;
-  uint32_t* bits_up;
+  uint4* bits;
   // live set
-  double* Lx[2];
-  double* Ly[2];
-  uint32_t* Lid[2];
-  uint32_t* Lseg[2];
-  // segment tables
+  double2* Lxy[2];
+  uint2* Lis[2];          // (id, segment)
+  // head tables
   double* Tx[2];
   double* Ty[2];
   uint32_t* Tid[2];
-  unsigned long long* Sd[2];
-  uint32_t* Sw[2];
+  // farthest-point slots
+  unsigned long long* Sd[3];
+  uint32_t* Sw[3];
   Route* route;
-  // output
-  double* out_x;
-  double* out_y;
-  uint32_t* out_id;
 };
 
 }  // namespace shb

@@ -21,21 +21,25 @@
 #include "hull_kernels.cuh"
 
 namespace shb {
-size_t k3_smem_bytes();
-cudaError_t configure_kernels();
-int k3_blocks_per_sm();
-void launch_k1(const Bufs& B, int grid, cudaStream_t s);
-void launch_k2(const Bufs& B, bool filter, int grid, int reverse, cudaStream_t s);
-void launch_k3(const Bufs& B, bool first, int grid, cudaStream_t s);
-void launch_k4(const Bufs& B, int grid, cudaStream_t s);
-void launch_k5(const double* Tx, const double* Ty, const uint32_t* Tid, uint32_t h, double* ox,
-               double* oy, long long* oidx, cudaStream_t s);
+void launch_k1(const Bufs& B, bool ids, bool vec, int grid, cudaStream_t s);
+void launch_k2(const Bufs& B, bool filter, bool ids, bool vec, int grid, cudaStream_t s);
+void launch_k3(const Bufs& B, bool ids, bool vec, int grid, cudaStream_t s);
+size_t rounds_smem_bytes();
+cudaError_t configure_round_kernels();
+int rounds_blocks_per_sm();
+cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s);
+void launch_k5(const Bufs& B, double* ox, double* oy, long long* oidx, uint64_t cap,
+               cudaStream_t s);
 void launch_gen_uniform(double* x, double* y, unsigned long long first, unsigned long long count,
                         unsigned long long seed, int grid, cudaStream_t s);
 void launch_gen_disk(double* x, double* y, unsigned long long n, unsigned long long seed,
                      unsigned long long cand0, uint32_t ncand, unsigned long long out_base,
                      Ctl* c, unsigned long long* status, uint32_t* epoch, int grid,
                      cudaStream_t s);
+int gen_tile_points();
+int k1_blocks_per_sm();
+int k2_blocks_per_sm();
+int k3_blocks_per_sm();
 }  // namespace shb
 
 using namespace shb;
@@ -56,7 +60,8 @@ struct CudaFail {
 struct DeviceInfo {
   int sm_count = 0;
   bool configured = false;
-  int k3_bps = 1;
+  int rounds_bps = 1;  // co-resident CTAs of the cooperative round kernel per SM
+  int k1_bps = 1, k2_bps = 1, k3_bps = 1;
 };
 
 std::mutex g_mutex;
@@ -75,7 +80,8 @@ struct Workspace {
   StatRec* h_stats = nullptr;  // pinned
   cudaEvent_t ev[8] = {};
   size_t tiles_cap = 0;
-  int k1_grid = 0, k2_grid = 0, k3_grid = 0, k4_grid = 0;
+  int stream_grid = 0, rounds_grid = 0;
+  int grid1 = 0, grid2 = 0, grid3 = 0;  // one full wave of each streaming kernel
 
   ~Workspace() {
     int cur = 0;
@@ -101,7 +107,10 @@ DeviceInfo& device_info(int device) {
   DeviceInfo& d = g_dev[device];
   if (!d.configured) {
     CK(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, device));
-    CK(configure_kernels());
+    CK(configure_round_kernels());
+    d.rounds_bps = rounds_blocks_per_sm();
+    d.k1_bps = k1_blocks_per_sm();
+    d.k2_bps = k2_blocks_per_sm();
     d.k3_bps = k3_blocks_per_sm();
     d.configured = true;
   }
@@ -125,11 +134,14 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   CK(cudaMallocHost((void**)&ws->h_stats, sizeof(StatRec) * STATS_CAP));
 
   const uint64_t N = std::max<uint64_t>(n_cap, 64), S = std::max<uint64_t>(s_cap, 64);
-  ws->k1_grid = (int)std::min<uint64_t>((N + TPB - 1) / TPB, (uint64_t)di.sm_count * 8);
-  ws->k2_grid = ws->k1_grid;
-  ws->k3_grid = di.sm_count * di.k3_bps;
-  ws->k4_grid = di.sm_count * 4;
-  ws->tiles_cap = std::max<uint64_t>((N + TILE - 1) / TILE, (S + 2047) / 2048) + 64;
+  // streaming kernels: 4 CTAs of 256 threads per SM; the round kernel: every
+  // co-resident CTA (cooperative launch)
+  ws->stream_grid = di.sm_count * 4;
+  ws->grid1 = di.sm_count * di.k1_bps;
+  ws->grid2 = di.sm_count * di.k2_bps;
+  ws->grid3 = di.sm_count * di.k3_bps;
+  ws->rounds_grid = std::min(di.sm_count * di.rounds_bps, MAX_ROUND_BLOCKS);
+  ws->tiles_cap = (N + gen_tile_points() - 1) / gen_tile_points() + 64;
 
   // carve one arena
   size_t off = 0;
@@ -140,29 +152,29 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   };
   const size_t o_ctl = take(sizeof(Ctl));
   const size_t o_epoch = take(sizeof(uint32_t));
-  const size_t o_k1 = take(sizeof(K1Partial) * ws->k1_grid);
+  const size_t o_k1 = take(sizeof(K1Partial) * std::max(ws->stream_grid, ws->grid1));
   const size_t o_stats = take(sizeof(StatRec) * STATS_CAP);
+  const size_t o_blk = take(sizeof(uint32_t) * 2 * MAX_ROUND_BLOCKS);
   const size_t o_tiles = take(sizeof(unsigned long long) * ws->tiles_cap);
-  const size_t words = (N + 31) / 32;
-  const size_t o_blo = take(4 * words), o_bup = take(4 * words);
-  size_t o_lx[2], o_ly[2], o_lid[2], o_lseg[2], o_tx[2], o_ty[2], o_tid[2], o_sd[2], o_sw[2];
+  const size_t o_bits = take(sizeof(uint4) * ((N + 63) / 64));
+  size_t o_lxy[2], o_lis[2], o_tx[2], o_ty[2], o_tid[2], o_sd[3], o_sw[3];
   for (int p = 0; p < 2; ++p) {
-    o_lx[p] = take(8 * N);
-    o_ly[p] = take(8 * N);
-    o_lid[p] = take(4 * N);
-    o_lseg[p] = take(4 * N);
+    o_lxy[p] = take(16 * N);
+    o_lis[p] = take(8 * N);
   }
   for (int p = 0; p < 2; ++p) {
     o_tx[p] = take(8 * S);
     o_ty[p] = take(8 * S);
     o_tid[p] = take(4 * S);
+  }
+  for (int p = 0; p < 3; ++p) {
     o_sd[p] = take(8 * S);
     o_sw[p] = take(4 * S);
   }
   const size_t o_route = take(sizeof(Route) * S);
   CK(cudaMalloc(&ws->arena, off));
   char* a = (char*)ws->arena;
-  CK(cudaMemset(a, 0, o_tiles + sizeof(unsigned long long) * ws->tiles_cap));
+  CK(cudaMemset(a, 0, o_bits));
   Bufs& B = ws->B;
   B.ctl = (Ctl*)(a + o_ctl);
   ws->epoch = B.epoch = (uint32_t*)(a + o_epoch);
@@ -170,17 +182,17 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   CK(cudaMemcpy(ws->epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
   B.k1part = (K1Partial*)(a + o_k1);
   B.stats = (StatRec*)(a + o_stats);
+  B.blk_cnt = (uint32_t*)(a + o_blk);
   B.tile_status = (unsigned long long*)(a + o_tiles);
-  B.bits_lo = (uint32_t*)(a + o_blo);
-  B.bits_up = (uint32_t*)(a + o_bup);
+  B.bits = (uint4*)(a + o_bits);
   for (int p = 0; p < 2; ++p) {
-    B.Lx[p] = (double*)(a + o_lx[p]);
-    B.Ly[p] = (double*)(a + o_ly[p]);
-    B.Lid[p] = (uint32_t*)(a + o_lid[p]);
-    B.Lseg[p] = (uint32_t*)(a + o_lseg[p]);
+    B.Lxy[p] = (double2*)(a + o_lxy[p]);
+    B.Lis[p] = (uint2*)(a + o_lis[p]);
     B.Tx[p] = (double*)(a + o_tx[p]);
     B.Ty[p] = (double*)(a + o_ty[p]);
     B.Tid[p] = (uint32_t*)(a + o_tid[p]);
+  }
+  for (int p = 0; p < 3; ++p) {
     B.Sd[p] = (unsigned long long*)(a + o_sd[p]);
     B.Sw[p] = (uint32_t*)(a + o_sw[p]);
   }
@@ -253,9 +265,11 @@ struct RunOut {
   std::string msg;
 };
 
-// Runs the pipeline; results stay in the workspace (h_ctl / device tables).
-RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, cudaStream_t st, bool timings,
-                    sh_phase_ms* ph) {
+// Runs the whole pipeline with ONE host synchronisation: H2D (host inputs),
+// K1, K2, K3, the cooperative round kernel, K5 (device outputs), and the
+// read-back of the control block + the first STATS_EAGER round stats.
+RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& res,
+                    cudaStream_t st, bool timings) {
   RunOut out;
   Bufs B = ws.B;
   const uint64_t n = rq.n;
@@ -273,50 +287,53 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, cudaStream_t st, b
     B.in_x = sx;
     B.in_y = sy;
     B.in_id = rq.ids ? sid : nullptr;
-    if (timings) CK(cudaEventRecord(ws.ev[1], st));
   } else {
-    if (timings) CK(cudaEventRecord(ws.ev[1], st));
     B.in_x = rq.x;
     B.in_y = rq.y;
     B.in_id = rq.ids;
   }
+  if (timings) CK(cudaEventRecord(ws.ev[1], st));
   B.n = (uint32_t)n;
+  const bool ids = B.in_id != nullptr;
+  // 16-byte pair loads need 16-byte aligned x/y (8-byte aligned ids)
+  const bool vec = ((uintptr_t)B.in_x % 16 == 0) && ((uintptr_t)B.in_y % 16 == 0) &&
+                   (!ids || (uintptr_t)B.in_id % 8 == 0);
 
   Ctl init;
   std::memset(&init, 0, sizeof(init));
   init.status = ST_RUNNING;
   init.n = (uint32_t)n;
-  init.s_cap = B.s_cap;
   init.mode = (uint32_t)rq.mode;
   *ws.h_ctl = init;
   CK(cudaMemcpyAsync(B.ctl, ws.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
 
-  const int g1 = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + TPB - 1) / TPB, ws.k1_grid));
-  launch_k1(B, g1, st);
+  auto grid_for = [&](int full) {
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)full));
+  };
+  launch_k1(B, ids, vec, grid_for(ws.grid1), st);
   if (timings) CK(cudaEventRecord(ws.ev[2], st));
-  launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, g1, /*reverse=*/1, st);
+  launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, ids, vec, grid_for(ws.grid2), st);
   if (timings) CK(cudaEventRecord(ws.ev[3], st));
-  launch_k3(B, true, ws.k3_grid, st);
-  out.launches = 3;
+  launch_k3(B, ids, vec, grid_for(ws.grid3), st);
   if (timings) CK(cudaEventRecord(ws.ev[4], st));
   CK(cudaGetLastError());
-
-  // rounds >= 2 in growing batches; each kernel exits at once when the
-  // device status is no longer RUNNING, so over-launching is harmless.
-  int batch = 6;
-  while (true) {
-    CK(cudaMemcpyAsync(ws.h_ctl, B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (ws.h_ctl->status != ST_RUNNING) break;
-    for (int k = 0; k < batch; ++k) {
-      launch_k4(B, ws.k4_grid, st);
-      launch_k3(B, false, ws.k3_grid, st);
-      out.launches += 2;
-    }
-    CK(cudaGetLastError());
-    batch = std::min(batch * 2, 64);
-  }
+  CK(launch_rounds(B, ws.rounds_grid, st));
+  out.launches = 4;
   if (timings) CK(cudaEventRecord(ws.ev[5], st));
+  const bool out_dev = (rq.flags & SH_OUT_DEVICE) != 0;
+  if (out_dev && (res.x || res.y || res.idx)) {
+    launch_k5(B, res.x, res.y, (long long*)res.idx, res.cap, st);
+    CK(cudaGetLastError());
+    out.launches += 1;
+  }
+  CK(cudaMemcpyAsync(ws.h_ctl, B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  const bool want_stats = res.stats && res.stats_cap && !(rq.flags & SH_NO_STATS);
+  if (want_stats)
+    CK(cudaMemcpyAsync(ws.h_stats, B.stats, sizeof(StatRec) * STATS_EAGER,
+                       cudaMemcpyDeviceToHost, st));
+  if (timings) CK(cudaEventRecord(ws.ev[6], st));
+  CK(cudaStreamSynchronize(st));
+
   const Ctl& c = *ws.h_ctl;
   out.rounds = c.round;
   out.kept = rq.mode == SH_MODE_WITH_PREPROCESS ? c.kept : n;
@@ -327,7 +344,7 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, cudaStream_t st, b
       break;
     case ST_SINGLE:
       out.h = 1;
-      out.kept = rq.mode == SH_MODE_WITH_PREPROCESS ? n : n;
+      out.kept = n;
       break;
     case ST_COLLINEAR:
       out.h = 2;
@@ -347,7 +364,6 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, cudaStream_t st, b
       out.code = SH_INTERNAL_ERROR;
       out.msg = "run: unexpected device status " + std::to_string(c.status);
   }
-  (void)ph;
   return out;
 }
 
@@ -380,12 +396,12 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
     ws = acquire(rq->device, n);
     const bool timings = (rq->flags & SH_PHASE_TIMINGS) != 0;
     cudaStream_t st = rq->stream ? (cudaStream_t)rq->stream : ws->stream;
-    RunOut o = run_pipeline(*ws, *rq, st, timings, &res->phases);
+    RunOut o = run_pipeline(*ws, *rq, *res, st, timings);
     if (o.code == -1) {  // segment tables too small: regrow to n + 2 and rerun
       const int dev = ws->device;
       ws.reset();
       ws = make_workspace(dev, std::max<uint64_t>(n, 1u << 12), n + 2);
-      o = run_pipeline(*ws, *rq, st, timings, &res->phases);
+      o = run_pipeline(*ws, *rq, *res, st, timings);
       if (o.code == -1) {
         o.code = SH_INTERNAL_ERROR;
         o.msg = "run: segment table overflow";
@@ -404,7 +420,6 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
       return o.code;
     }
     const Ctl& c = *ws->h_ctl;
-    // vertices
     if (o.h > res->cap && (res->x || res->y || res->idx)) {
       put_err(res->err, sizeof(res->err), "output capacity too small");
       release(std::move(ws));
@@ -412,35 +427,22 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
       return SH_CAP_TOO_SMALL;
     }
     const bool out_dev = (rq->flags & SH_OUT_DEVICE) != 0;
+    const bool want_stats = res->stats && res->stats_cap && !(rq->flags & SH_NO_STATS);
+    const uint64_t nst =
+        want_stats ? std::min<uint64_t>({o.rounds, (uint64_t)STATS_CAP, res->stats_cap}) : 0;
+    bool sync2 = false;
+    std::vector<uint32_t> ids;
     if (c.status == ST_DONE) {
-      const uint32_t par = c.parity;
-      const uint64_t nst = std::min<uint64_t>({o.rounds, (uint64_t)STATS_CAP, res->stats ? res->stats_cap : 0});
-      std::vector<uint32_t> ids;
-      if (out_dev) {
-        // vertices stay in HBM: one emit kernel (u32 ids -> i64) on the call's stream
-        if (o.h && (res->x || res->y || res->idx)) {
-          launch_k5(ws->B.Tx[par], ws->B.Ty[par], ws->B.Tid[par], (uint32_t)o.h, res->x, res->y,
-                    (long long*)res->idx, st);
-          CK(cudaGetLastError());
-          res->kernel_launches += 1;
-        }
-      } else {
+      // heads of the final table (CCW from P0); device outputs were written by K5
+      const uint32_t par = c.round & 1u;
+      if (!out_dev && o.h) {
         if (res->x) CK(cudaMemcpyAsync(res->x, ws->B.Tx[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
         if (res->y) CK(cudaMemcpyAsync(res->y, ws->B.Ty[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
         if (res->idx) {
           ids.resize(o.h);
           CK(cudaMemcpyAsync(ids.data(), ws->B.Tid[par], 4 * o.h, cudaMemcpyDeviceToHost, st));
         }
-      }
-      if (nst) CK(cudaMemcpyAsync(ws->h_stats, ws->B.stats, sizeof(StatRec) * nst, cudaMemcpyDeviceToHost, st));
-      if (timings) CK(cudaEventRecord(ws->ev[6], st));
-      CK(cudaStreamSynchronize(st));
-      for (uint64_t i = 0; !out_dev && res->idx && i < o.h; ++i) res->idx[i] = ids[i];
-      for (uint64_t i = 0; i < nst; ++i) {
-        res->stats[i].iteration = i + 1;
-        res->stats[i].segments = ws->h_stats[i].segments;
-        res->stats[i].points_remaining = ws->h_stats[i].points_remaining;
-        res->stats[i].points_removed = ws->h_stats[i].points_removed;
+        sync2 = true;
       }
     } else {
       // degenerate: {lo} or {lo, hi} (hull.cpp:234-248)
@@ -456,6 +458,7 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
         if (res->x) CK(cudaMemcpyAsync(res->x, vx, 8 * o.h, cudaMemcpyHostToDevice, st));
         if (res->y) CK(cudaMemcpyAsync(res->y, vy, 8 * o.h, cudaMemcpyHostToDevice, st));
         if (res->idx) CK(cudaMemcpyAsync(res->idx, vi, 8 * o.h, cudaMemcpyHostToDevice, st));
+        sync2 = true;
       } else {
         for (uint64_t i = 0; i < o.h; ++i) {
           if (res->x) res->x[i] = vx[i];
@@ -463,8 +466,19 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
           if (res->idx) res->idx[i] = vi[i];
         }
       }
-      if (timings) CK(cudaEventRecord(ws->ev[6], st));
-      CK(cudaStreamSynchronize(st));
+    }
+    if (nst > (uint64_t)STATS_EAGER) {
+      CK(cudaMemcpyAsync(ws->h_stats + STATS_EAGER, ws->B.stats + STATS_EAGER,
+                         sizeof(StatRec) * (nst - STATS_EAGER), cudaMemcpyDeviceToHost, st));
+      sync2 = true;
+    }
+    if (sync2) CK(cudaStreamSynchronize(st));
+    for (uint64_t i = 0; !out_dev && res->idx && i < ids.size(); ++i) res->idx[i] = ids[i];
+    for (uint64_t i = 0; i < nst; ++i) {
+      res->stats[i].iteration = i + 1;
+      res->stats[i].segments = ws->h_stats[i].segments;
+      res->stats[i].points_remaining = ws->h_stats[i].points_remaining;
+      res->stats[i].points_removed = ws->h_stats[i].points_removed;
     }
     if (timings) {
       auto el = [&](int i, int j) {
@@ -567,13 +581,13 @@ int sh_b200_gen_disk(double* x, double* y, uint64_t n, uint64_t seed, int device
     *ws->h_ctl = init;
     CK(cudaMemcpyAsync(ws->B.ctl, ws->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
     uint64_t accepted = 0, cand0 = 0;
-    const uint64_t max_batch = (uint64_t)(ws->tiles_cap - 64) * TILE;
+    const uint64_t max_batch = (uint64_t)(ws->tiles_cap - 64) * gen_tile_points();
     while (accepted < n) {
       const uint64_t need = n - accepted;
       uint64_t batch = need + need / 4 + 4096;
       batch = std::min<uint64_t>(batch, max_batch);
       launch_gen_disk(x, y, n, seed, cand0, (uint32_t)batch, accepted, ws->B.ctl,
-                      ws->B.tile_status, ws->epoch, ws->k3_grid, st);
+                      ws->B.tile_status, ws->epoch, ws->stream_grid, st);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(ws->h_ctl, ws->B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));

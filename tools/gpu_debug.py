@@ -42,6 +42,15 @@ for n, s in [(1000, 1), (100000, 42), (1000000, 1)]:
     for m in (1, 2): allok &= cmp(f"uniform{n}", x, y, m)
 x, y = dataio.gen_circle(200000, 3)
 allok &= cmp("circle200k", x, y, 1)
+allok &= cmp("circle200k", x, y, 2)
+x, y = dataio.gen_circle(1_000_000, 1)
+allok &= cmp("circle1M", x, y, 1)
+x, y = oracle.gen_disk(2_000_000, 1)
+allok &= cmp("disk2M", x, y, 1)
+rng = np.random.default_rng(5)
+g = rng.integers(0, 40, size=(300000, 2)).astype(np.float64)
+allok &= cmp("grid40_300k", g[:, 0].copy(), g[:, 1].copy(), 1)
+allok &= cmp("grid40_300k", g[:, 0].copy(), g[:, 1].copy(), 2)
 x, y = dataio.gen_uniform(20_000_000, 1)
 for i in range(3): allok &= cmp("uniform20M", x, y, 1)
 print("ALL OK" if allok else "FAILURES")
