@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SH_B200_ABI_VERSION 1
+#define SH_B200_ABI_VERSION 2
 
 /* return codes: 0 or 1 + seghull::Errc (error.hpp:8-19) */
 enum sh_status {
@@ -62,12 +62,13 @@ enum sh_flags {
                           /* the vertices never leave HBM (shard hulls -> gather)    */
 };
 
-/* hull.hpp:35-40 SegmentStats */
+/* hull.hpp:35-40 SegmentStats, plus the device time at which the round ended */
 typedef struct {
   uint64_t iteration;
   uint64_t segments;
   uint64_t points_remaining;
   uint64_t points_removed;
+  uint64_t end_ns;  /* %globaltimer at the end of the round, relative to the start of K1 */
 } sh_round_stat;
 
 /* hull.hpp:42-46 PhaseTimings (device time from CUDA events) */

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libseghull_b200.so")
+LIB_PATH = os.environ.get("SHB_LIB") or os.path.join(HERE, "libseghull_b200.so")
 
 _u64 = ctypes.c_uint64
 _u32 = ctypes.c_uint32
@@ -20,7 +20,7 @@ _vp = ctypes.c_void_p
 
 class sh_round_stat(ctypes.Structure):
     _fields_ = [("iteration", _u64), ("segments", _u64),
-                ("points_remaining", _u64), ("points_removed", _u64)]
+                ("points_remaining", _u64), ("points_removed", _u64), ("end_ns", _u64)]
 
 
 class sh_phase_ms(ctypes.Structure):

@@ -10,6 +10,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "hull_kernels.cuh"
+
 #define SH_DEV __device__ __forceinline__
 
 namespace shb {
@@ -133,6 +135,12 @@ SH_DEV uint32_t ld_relaxed_u32(const uint32_t* p) {
   return v;
 }
 
+SH_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 SH_DEV uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -140,61 +148,69 @@ SH_DEV uint32_t lanemask_lt() {
 }
 
 // ---------------------------------------------------------------------------
-// Farthest-point slot {dbits, win}: a 64-bit atomicMax on the distance bits
-// (positive doubles order like their bit patterns) filters contention, then a
-// CAS loop on the winner's position applies the full comparator.  The
-// incumbent's distance is recomputed from its stored coordinates against the
-// slot's edge -- every contender of a slot belongs to the same new segment,
-// so the caller's own edge IS the slot's edge and the recomputed value is
-// bit-identical to the one the incumbent offered.
-//   LD : functor (pos) -> (x, y, id) reading the array the positions index
-// Callers must have made the candidate's own row visible (__threadfence)
-// before offering.  Works on global and on shared slots (generic atomics).
-template <class LD>
-SH_DEV void slot_offer(unsigned long long* dbits, uint32_t* win, const Cand& c, bool lower,
-                       const Edge& e, const LD& ld) {
+// Farthest-point slot {dbits, SlotRec}: a 64-bit atomicMax on the distance
+// bits (positive doubles order like their bit patterns) filters contention;
+// only contenders that reach the running maximum take the record's lock and
+// apply the full comparator.  Works on global and shared slots (generic
+// atomics).  The lock loop keeps the critical section inside the loop body,
+// which is starvation-free under independent thread scheduling even when two
+// lanes of one warp contend.
+// SHARED: the record lives in shared memory (CTA-scope ordering suffices);
+// otherwise gpu scope with acquire/release fences (not the sequentially
+// consistent __threadfence, which also invalidates L1).
+SH_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+template <bool SHARED>
+SH_DEV void rec_update(SlotRec* rec, const Cand& c, bool lower) {
+  bool done = false;
+  while (!done) {
+    if (atomicCAS(&rec->lock, 0u, 1u) == 0u) {
+      if (SHARED) __threadfence_block(); else fence_acq_rel_gpu();
+      volatile SlotRec* v = rec;
+      Cand o;
+      o.id = v->id;
+      o.d = v->d;
+      o.x = v->x;
+      o.y = v->y;
+      if (o.id == NONE || cand_better(c, o, lower)) {
+        v->d = c.d;
+        v->x = c.x;
+        v->y = c.y;
+        v->id = c.id;
+      }
+      if (SHARED) __threadfence_block(); else fence_acq_rel_gpu();
+      atomicExch(&rec->lock, 0u);
+      done = true;
+    }
+  }
+}
+
+// global slot offer (the record is read by other CTAs / the next round)
+SH_DEV void rec_offer(unsigned long long* dbits, SlotRec* rec, const Cand& c, bool lower) {
   const unsigned long long mine = (unsigned long long)__double_as_longlong(c.d);
   if (mine < *(volatile unsigned long long*)dbits) return;
   const unsigned long long old = atomicMax(dbits, mine);
   if (mine < old) return;
-  uint32_t cur = *(volatile uint32_t*)win;
-  while (true) {
-    if (cur != NONE) {
-      Cand o;
-      ld(cur, o.x, o.y, o.id);
-      o.d = outward_e(e, o.x, o.y);
-      o.pos = cur;
-      if (!cand_better(c, o, lower)) return;
-    }
-    const uint32_t prev = atomicCAS(win, cur, c.pos);
-    if (prev == cur) return;
-    cur = prev;
-  }
+  rec_update<false>(rec, c, lower);
 }
 
-// (x, y, id) of a position in SoA input arrays (ids null => id == position)
-struct LoadSoA {
-  const double* x;
-  const double* y;
-  const uint32_t* id;
-  SH_DEV void operator()(uint32_t p, double& ox, double& oy, uint32_t& oid) const {
-    ox = __ldcg(x + p);
-    oy = __ldcg(y + p);
-    oid = id ? __ldcg(id + p) : p;
-  }
-};
+// relaxed gpu-scope atomic add issued from one lane: inline PTX so the
+// compiler cannot turn it into a warp-aggregated atomic whose result is
+// shuffled (and therefore waited for) right away
+SH_DEV uint32_t atom_add_relaxed(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 
-// (x, y, id) of a position in a live set
-struct LoadLive {
-  const double2* xy;
-  const uint2* is;
-  SH_DEV void operator()(uint32_t p, double& ox, double& oy, uint32_t& oid) const {
-    const double2 v = __ldcg(xy + p);
-    ox = v.x;
-    oy = v.y;
-    oid = __ldcg(&is[p].x);
-  }
-};
+SH_DEV void rec_clear(unsigned long long* dbits, SlotRec* rec) {
+  *dbits = 0ull;
+  rec->d = 0.0;
+  rec->x = 0.0;
+  rec->y = 0.0;
+  rec->id = NONE;
+  rec->lock = 0u;
+}
 
 // ---------------------------------------------------------------------------
 // Grid barrier for a cooperative launch (all CTAs co-resident).  The
@@ -209,10 +225,10 @@ SH_DEV void grid_barrier(uint32_t* count, uint32_t* gen, uint32_t nblocks) {
   if (threadIdx.x == 0) {
     uint32_t g;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
-    __threadfence();
+    fence_acq_rel_gpu();
     if (atomicAdd(count, 1u) == nblocks - 1) {
       *(volatile uint32_t*)count = 0u;
-      __threadfence();
+      fence_acq_rel_gpu();
       st_release_u32(gen, g + 1);
     } else {
       uint32_t v;
@@ -222,7 +238,7 @@ SH_DEV void grid_barrier(uint32_t* count, uint32_t* gen, uint32_t nblocks) {
         __nanosleep(20);
       }
     }
-    __threadfence();
+    fence_acq_rel_gpu();
   }
   __syncthreads();
 }
@@ -310,6 +326,143 @@ SH_DEV uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32_t* 
   const uint32_t r = before + x - v;
   __syncthreads();
   return r;
+}
+
+}  // namespace shb
+
+// ---------------------------------------------------------------------------
+// TMA bulk-copy ring (sm_90+/sm_100a `cp.async.bulk` + mbarrier transaction
+// counts).  One elected thread streams fixed-size tiles of the SoA input into
+// NS shared-memory stages; every thread consumes a stage after waiting on its
+// mbarrier phase.  The memory system always has NS-1 tiles in flight per CTA
+// regardless of how long the consumers compute, which is what the latency-
+// bound register-load versions of K1/K2/K3 lacked (ncu: 0.5-0.7 eligible
+// warps per scheduler at 25-37% occupancy).
+namespace shb {
+
+SH_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+SH_DEV void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+SH_DEV void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+SH_DEV void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+SH_DEV void tma_load_1d(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+SH_DEV void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Ring of NS stages of T points (x, y f64 and optionally ids u32).
+// T % 64 == 0; the global arrays must be 16-byte aligned (the host stages
+// unaligned inputs).  A tile's last (cnt % 4) points are not copied (bulk
+// copies move multiples of 16 bytes); consumers read those from global.
+template <int T, int NS, bool IDS, int AUX = 0>
+struct TileRing {
+  // AUX: bytes per 64-point chunk of an optional side stream (K3: the chain bits)
+  static constexpr size_t kAuxBytes = (size_t)(T / 64) * AUX;
+  static constexpr size_t kStageBytes = (size_t)T * (16 + (IDS ? 4 : 0)) + kAuxBytes;
+  static constexpr size_t kBytes = NS * kStageBytes + NS * sizeof(unsigned long long);
+  double* xs;                 // [NS][T]
+  double* ys;                 // [NS][T]
+  uint32_t* is;               // [NS][T] when IDS
+  unsigned char* aux;         // [NS][kAuxBytes]
+  unsigned long long* bar;    // [NS]
+
+  SH_DEV void carve(unsigned char* base) {
+    xs = reinterpret_cast<double*>(base);
+    ys = xs + NS * T;
+    is = reinterpret_cast<uint32_t*>(ys + NS * T);
+    aux = reinterpret_cast<unsigned char*>(is + (IDS ? NS * T : 0));
+    bar = reinterpret_cast<unsigned long long*>(base + NS * kStageBytes);
+  }
+  SH_DEV void init() {  // thread 0, followed by __syncthreads by the caller
+    for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
+    mbar_fence_init();
+  }
+  // thread 0: stream points [first, first + cnt) into stage s
+  SH_DEV void issue(int s, const double* X, const double* Y, const uint32_t* I, uint32_t first,
+                    uint32_t cnt, const unsigned char* A = nullptr) {
+    const uint32_t c4 = cnt & ~3u;
+    const uint32_t ab = AUX ? ((cnt + 63) / 64) * AUX : 0u;
+    if (c4 == 0 && ab == 0) {  // nothing to copy: complete the phase with a plain arrival
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar + s))
+                   : "memory");
+      return;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // stage was read by threads
+    mbar_expect_tx(bar + s, c4 * (16u + (IDS ? 4u : 0u)) + ab);
+    if (c4) {
+      tma_load_1d(xs + s * T, X + first, c4 * 8u, bar + s);
+      tma_load_1d(ys + s * T, Y + first, c4 * 8u, bar + s);
+      if (IDS) tma_load_1d(is + s * T, I + first, c4 * 4u, bar + s);
+    }
+    if (ab) tma_load_1d(aux + s * kAuxBytes, A + (size_t)(first / 64) * AUX, ab, bar + s);
+  }
+  SH_DEV void wait(int s, uint32_t parity) { mbar_wait(bar + s, parity); }
+};
+
+}  // namespace shb
+
+namespace shb {
+
+// Streams this CTA's share of the input through the ring: tiles b, b+G, ...
+// (mapped to ntiles-1-t when `reverse`), calling body(stage, first, cnt) for
+// each after its bytes landed.  A __syncthreads follows each body before the
+// stage is refilled.  The caller initialised the ring (+ __syncthreads).
+template <int T, int NS, bool IDS, int AUX, class Body>
+SH_DEV void stream_input(TileRing<T, NS, IDS, AUX>& R, uint32_t n, const double* X,
+                         const double* Y, const uint32_t* I, const unsigned char* A, bool reverse,
+                         const Body& body) {
+  const uint32_t ntiles = (n + T - 1) / T;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t mine = b < ntiles ? (ntiles - 1 - b) / G + 1 : 0;
+  auto tile_of = [&](uint32_t k) {
+    const uint32_t t = b + k * G;
+    return reverse ? ntiles - 1 - t : t;
+  };
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < mine && k < (uint32_t)NS; ++k) {
+      const uint32_t first = tile_of(k) * T;
+      R.issue((int)k, X, Y, I, first, min((uint32_t)T, n - first), A);
+    }
+  }
+  for (uint32_t k = 0; k < mine; ++k) {
+    const int s = (int)(k % NS);
+    R.wait(s, (k / NS) & 1u);
+    const uint32_t first = tile_of(k) * T;
+    body(s, first, min((uint32_t)T, n - first));
+    __syncthreads();
+    if (threadIdx.x == 0 && k + NS < mine) {
+      const uint32_t f2 = tile_of(k + NS) * T;
+      R.issue(s, X, Y, I, f2, min((uint32_t)T, n - f2), A);
+    }
+  }
 }
 
 }  // namespace shb

@@ -7,9 +7,12 @@
 //   chain bits   uint4[ceil(n/64)]: K2's per-point class for one 64-point
 //                chunk {lower even, lower odd, upper even, upper odd}; bit l of
 //                word "even" is point 64c+2l, of "odd" point 64c+2l+1
-//   live set     ping-pong {xy double2, (id, seg) uint2}[n]      24 B/point
+//   live set     ping-pong {xy double2, (id, seg) uint2}[cap]    24 B/point,
+//                organised as RUNS: run j occupies [j*run_q, j*run_q + cnt_j);
+//                CTA j of a round writes its survivors densely into run j
+//                (CTA-local offsets, no global atomics), run_cnt[par][j] = cnt_j
 //   head table   ping-pong {x f64, y f64, id u32}[S]              20 B/segment
-//   farthest     3-way rotating slots {dbits u64, win u32}[S]     12 B/segment
+//   farthest     3-way rotating slots {dbits u64, SlotRec 32 B}[S] 40 B/segment
 //   route table  Route[S] 64 B (large tables only; small ones live in smem)
 //
 // Round numbering follows hull.cpp:264-282: round r >= 1 splits the
@@ -19,8 +22,8 @@
 //   round r reads  heads Tab[(r-1)&1], farthest slots Slot[(r-1)%3],
 //                  live set Live[(r-1)&1] (round 1: the input)
 //   round r writes heads Tab[r&1], slots Slot[r%3] (next round's farthest
-//                  points), live set Live[r&1], survivor count out_cnt[r%3]
-//   round r clears Slot[(r+1)%3] and out_cnt[(r+1)%3] for round r+1
+//                  points), live set Live[r&1] + its run counts
+//   round r clears Slot[(r+1)%3] for round r+1
 // so no buffer is ever cleared while another CTA may still read it.
 #pragma once
 
@@ -31,12 +34,24 @@ namespace shb {
 constexpr int TPB = 256;             // K1 / K2 / K3 (streaming kernels)
 constexpr int WARPS = TPB / 32;
 constexpr int RTPB = 512;            // persistent round kernel
+constexpr int STPB = 512;            // TMA-fed streaming kernels K1/K2/K3 (one CTA per SM)
+constexpr int SWARPS = STPB / 32;
+#ifndef SHB_STREAM_T
+#define SHB_STREAM_T 2048
+#endif
+#ifndef SHB_STREAM_NS
+#define SHB_STREAM_NS 4
+#endif
+constexpr int STREAM_T = SHB_STREAM_T;    // points per TMA tile
+constexpr int STREAM_NS = SHB_STREAM_NS;  // ring stages (NS-1 tiles in flight while one is consumed)
 constexpr int SMALL_S = 1024;        // tables up to this size are rebuilt per CTA in smem
 constexpr int NSLOT = 2 * SMALL_S;   // next-round segments of a small table
 constexpr uint32_t TAIL_M = 4096;    // live sets up to this size finish in one CTA
 constexpr int STATS_CAP = 1 << 16;
 constexpr int STATS_EAGER = 64;      // stats read back together with the control block
 constexpr int MAX_ROUND_BLOCKS = 1024;
+constexpr int MAX_RUNS = MAX_ROUND_BLOCKS;
+constexpr int CLIST = 256;           // phase-B contender list entries per tile
 
 enum Status : uint32_t {
   ST_RUNNING = 0,
@@ -69,8 +84,20 @@ struct __align__(16) Route {
 };
 constexpr uint32_t RT_SPLIT = 1u, RT_LOWER = 2u;
 
+// Farthest-point record of one segment slot: the best candidate so far
+// under the full comparator (d, then chain-lex, then id).  Updated under
+// `lock` by the rare contenders that reach the slot's running maximum
+// distance (dbits); C's coordinates are read straight from here by the next
+// round's table phase.
+struct __align__(16) SlotRec {
+  double d, x, y;
+  uint32_t id;    // NONE: no candidate (segment not splittable)
+  uint32_t lock;
+};
+
 struct StatRec {
   uint32_t segments, points_remaining, points_removed, pad;
+  unsigned long long end_ns;  // %globaltimer at the end of the round (minus Ctl::t0_ns)
 };
 
 // Device-resident control block.  The host writes it once per call and
@@ -91,12 +118,13 @@ struct Ctl {
   unsigned long long kept;
   uint32_t noncollinear;
   uint32_t ticket;      // last-CTA ticket of K1 / K2 / K3
-  uint32_t out_cnt[3];  // survivors of round r accumulate in out_cnt[r % 3]
+  uint32_t nruns;       // runs of the live set after `round`
   uint32_t bar_count;   // grid barrier of the round kernel
   uint32_t bar_gen;
   uint32_t mode;
   uint32_t tile_ctr;    // generator scratch
   uint32_t m_next;      // generator scratch
+  unsigned long long t0_ns;  // %globaltimer when K1 started (per-round timestamps)
 };
 
 struct Bufs {
@@ -115,16 +143,18 @@ struct Bufs {
   uint32_t* blk_cnt;      // [2 * MAX_ROUND_BLOCKS] per-CTA counts of a large table scan
   // classification bits
   uint4* bits;
-  // live set
+  // live set (runs)
   double2* Lxy[2];
   uint2* Lis[2];          // (id, segment)
+  uint32_t* run_cnt[2];   // [MAX_RUNS] survivors per run
+  uint32_t run_q;         // run stride in points
   // head tables
   double* Tx[2];
   double* Ty[2];
   uint32_t* Tid[2];
   // farthest-point slots
   unsigned long long* Sd[3];
-  uint32_t* Sw[3];
+  SlotRec* Srec[3];
   Route* route;
 };
 

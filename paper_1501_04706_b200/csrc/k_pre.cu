@@ -25,21 +25,18 @@ namespace shb {
 // helpers
 // ===========================================================================
 
+// Total order of doubles as u64 keys (-0.0 sorts just below +0.0; a
+// threshold only has to bound the final extreme, so that is harmless).
+SH_DEV unsigned long long okey(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+SH_DEV double okey_dec(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
 SH_DEV bool nonfinite(double v) {
   return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
-}
-
-// pair q = points (2q, 2q+1) of a SoA array
-template <bool VEC>
-SH_DEV double2 load_pair(const double* __restrict__ a, uint32_t q) {
-  if (VEC) return __ldg(reinterpret_cast<const double2*>(a) + q);
-  return make_double2(__ldg(a + 2 * q), __ldg(a + 2 * q + 1));
-}
-
-template <bool VEC>
-SH_DEV uint2 load_pair_id(const uint32_t* __restrict__ a, uint32_t q) {
-  if (VEC) return __ldg(reinterpret_cast<const uint2*>(a) + q);
-  return make_uint2(__ldg(a + 2 * q), __ldg(a + 2 * q + 1));
 }
 
 // ===========================================================================
@@ -94,8 +91,8 @@ SH_DEV void warp_reduce_ext(ExtRec* e, unsigned long long& bad) {
 
 // reduce (e, bad) over the block; result valid in thread 0
 SH_DEV void block_reduce_ext(ExtRec* e, unsigned long long& bad) {
-  __shared__ ExtRec s_e[4][WARPS];
-  __shared__ unsigned long long s_bad[WARPS];
+  __shared__ ExtRec s_e[4][SWARPS];
+  __shared__ unsigned long long s_bad[SWARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   warp_reduce_ext(e, bad);
   if (lane == 0) {
@@ -105,13 +102,13 @@ SH_DEV void block_reduce_ext(ExtRec* e, unsigned long long& bad) {
   __syncthreads();
   if (warp == 0) {
     for (int k = 0; k < 4; ++k) {
-      if (lane < WARPS) {
+      if (lane < SWARPS) {
         e[k] = s_e[k][lane];
       } else {
         e[k].pos = NONE;
       }
     }
-    bad = lane < WARPS ? s_bad[lane] : ~0ull;
+    bad = lane < SWARPS ? s_bad[lane] : ~0ull;
     warp_reduce_ext(e, bad);
   }
   __syncthreads();
@@ -141,10 +138,14 @@ SH_DEV void ext_visit(ExtRec (&e)[4], unsigned long long& bad, double x, double 
   }
 }
 
-constexpr int K1_U = 4;  // pairs per thread per iteration: 4 x 2 x 16 B in flight
+using Ring = TileRing<STREAM_T, STREAM_NS, false>;
+using RingI = TileRing<STREAM_T, STREAM_NS, true>;
 
-template <bool IDS, bool VEC>
-__global__ void __launch_bounds__(TPB) k1_extremes(Bufs B) {
+template <bool IDS>
+__global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TileRing<STREAM_T, STREAM_NS, IDS> R;
+  R.carve(smem_raw);
   Ctl* c = B.ctl;
   const uint32_t n = B.n;
   const double* __restrict__ X = B.in_x;
@@ -158,36 +159,72 @@ __global__ void __launch_bounds__(TPB) k1_extremes(Bufs B) {
   e[3].x = INF;  e[3].y = -INF;  // top
   for (int k = 0; k < 4; ++k) e[k].id = e[k].pos = NONE;
   unsigned long long bad = ~0ull;
+  if (blockIdx.x == 0 && threadIdx.x == 0) c->t0_ns = globaltimer_ns();
+  // CTA-wide thresholds for the branch-free filter: a point can only become
+  // an extreme if it is at least as extreme as the CTA's running extreme
+  // (which bounds the final one).  Keys: min x, min y, max x, max y.
+  __shared__ unsigned long long s_thr[4];
+  if (threadIdx.x == 0) {
+    R.init();
+    s_thr[0] = okey(INF);
+    s_thr[1] = okey(INF);
+    s_thr[2] = okey(-INF);
+    s_thr[3] = okey(-INF);
+  }
+  __syncthreads();
 
-  const uint32_t npairs = n >> 1;
-  const uint32_t stride = gridDim.x * TPB;
-  uint32_t q = blockIdx.x * TPB + threadIdx.x;
-  for (; q + (K1_U - 1) * stride < npairs; q += K1_U * stride) {
-    double2 xv[K1_U], yv[K1_U];
-    uint2 iv[K1_U];
+  // forward over the input; within a thread indices only grow, so strict
+  // comparisons keep the lowest index among exact duplicates
+  stream_input(R, n, X, Y, I, nullptr, false, [&](int s, uint32_t first, uint32_t cnt) {
+    const double* xs = R.xs + s * STREAM_T;
+    const double* ys = R.ys + s * STREAM_T;
+    const uint32_t* is = R.is + s * STREAM_T;
+    const double t0 = okey_dec(*(volatile unsigned long long*)&s_thr[0]);
+    const double t1 = okey_dec(*(volatile unsigned long long*)&s_thr[1]);
+    const double t2 = okey_dec(*(volatile unsigned long long*)&s_thr[2]);
+    const double t3 = okey_dec(*(volatile unsigned long long*)&s_thr[3]);
+    bool moved = false;
+    if (cnt == (uint32_t)STREAM_T) {
 #pragma unroll
-    for (int u = 0; u < K1_U; ++u) {
-      xv[u] = load_pair<VEC>(X, q + u * stride);
-      yv[u] = load_pair<VEC>(Y, q + u * stride);
-      if (IDS) iv[u] = load_pair_id<VEC>(I, q + u * stride);
+      for (int k = 0; k < STREAM_T / 2 / STPB; ++k) {
+        const uint32_t p = k * STPB + threadIdx.x;
+        const double2 xv = reinterpret_cast<const double2*>(xs)[p];
+        const double2 yv = reinterpret_cast<const double2*>(ys)[p];
+        // can either point reach an extreme, or is it non-finite (exponent
+        // all ones)?  Rare once the CTA thresholds have settled.
+        const uint32_t M = 0x7ff00000u;
+        const uint32_t hm = max(max((uint32_t)__double2hiint(xv.x) & M, (uint32_t)__double2hiint(xv.y) & M),
+                                max((uint32_t)__double2hiint(yv.x) & M, (uint32_t)__double2hiint(yv.y) & M));
+        const bool cand = (hm == M) | (xv.x <= t0) | (xv.y <= t0) | (yv.x <= t1) | (yv.y <= t1) |
+                          (xv.x >= t2) | (xv.y >= t2) | (yv.x >= t3) | (yv.y >= t3);
+        if (cand) {
+          uint2 iv = make_uint2(0u, 0u);
+          if (IDS) iv = reinterpret_cast<const uint2*>(is)[p];
+          const uint32_t i = first + 2 * p;
+          ext_visit<IDS>(e, bad, xv.x, yv.x, IDS ? iv.x : i, i);
+          ext_visit<IDS>(e, bad, xv.y, yv.y, IDS ? iv.y : i + 1, i + 1);
+          moved = true;
+        }
+      }
+    } else {
+      const uint32_t c4 = cnt & ~3u;
+      for (uint32_t j = threadIdx.x; j < cnt; j += STPB) {
+        const uint32_t i = first + j;
+        const bool sm = j < c4;
+        const double x = sm ? xs[j] : __ldg(X + i);
+        const double y = sm ? ys[j] : __ldg(Y + i);
+        const uint32_t id = IDS ? (sm ? is[j] : __ldg(I + i)) : i;
+        ext_visit<IDS>(e, bad, x, y, id, i);
+      }
+      moved = true;
     }
-#pragma unroll
-    for (int u = 0; u < K1_U; ++u) {
-      const uint32_t p = 2 * (q + u * stride);
-      ext_visit<IDS>(e, bad, xv[u].x, yv[u].x, IDS ? iv[u].x : p, p);
-      ext_visit<IDS>(e, bad, xv[u].y, yv[u].y, IDS ? iv[u].y : p + 1, p + 1);
+    if (moved) {  // publish this thread's extremes as CTA thresholds
+      if (e[0].pos != NONE) atomicMin(&s_thr[0], okey(e[0].x));
+      if (e[1].pos != NONE) atomicMin(&s_thr[1], okey(e[1].y));
+      if (e[2].pos != NONE) atomicMax(&s_thr[2], okey(e[2].x));
+      if (e[3].pos != NONE) atomicMax(&s_thr[3], okey(e[3].y));
     }
-  }
-  for (; q < npairs; q += stride) {
-    const double2 xv = load_pair<VEC>(X, q), yv = load_pair<VEC>(Y, q);
-    const uint32_t p = 2 * q;
-    ext_visit<IDS>(e, bad, xv.x, yv.x, IDS ? __ldg(I + p) : p, p);
-    ext_visit<IDS>(e, bad, xv.y, yv.y, IDS ? __ldg(I + p + 1) : p + 1, p + 1);
-  }
-  if ((n & 1u) && blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint32_t p = n - 1;
-    ext_visit<IDS>(e, bad, __ldg(X + p), __ldg(Y + p), IDS ? __ldg(I + p) : p, p);
-  }
+  });
 
   block_reduce_ext(e, bad);
   __shared__ int s_last;
@@ -206,7 +243,7 @@ __global__ void __launch_bounds__(TPB) k1_extremes(Bufs B) {
   // last CTA: combine the per-CTA partials
   for (int k = 0; k < 4; ++k) e[k].pos = NONE;
   bad = ~0ull;
-  for (uint32_t p = threadIdx.x; p < gridDim.x; p += TPB) {
+  for (uint32_t p = threadIdx.x; p < gridDim.x; p += STPB) {
     const K1Partial* qp = B.k1part + p;
     ExtRec o[4];
     for (int k = 0; k < 4; ++k) {
@@ -228,10 +265,8 @@ __global__ void __launch_bounds__(TPB) k1_extremes(Bufs B) {
   c->ticket = 0;
   c->bad_index = bad;
   // round-0 farthest slots (K2 offers into Slot[0]; hull_kernels.cuh)
-  B.Sd[0][0] = 0ull;
-  B.Sd[0][1] = 0ull;
-  B.Sw[0][0] = NONE;
-  B.Sw[0][1] = NONE;
+  rec_clear(&B.Sd[0][0], &B.Srec[0][0]);
+  rec_clear(&B.Sd[0][1], &B.Srec[0][1]);
   if (bad != ~0ull) {
     c->status = ST_NONFINITE;
     return;
@@ -277,8 +312,6 @@ __global__ void __launch_bounds__(TPB) k1_extremes(Bufs B) {
 // K2: filter + classification + round-0 farthest points (no point writes).
 // ===========================================================================
 
-constexpr int K2_U = 2;  // 64-point chunks per warp per iteration (8 x 16 B per lane in flight)
-
 SH_DEV void cand_visit(Cand& a, double d, double x, double y, uint32_t id, uint32_t pos,
                        bool lower) {
   if (d > 0.0 && d >= a.d) {
@@ -288,8 +321,11 @@ SH_DEV void cand_visit(Cand& a, double d, double x, double y, uint32_t id, uint3
   }
 }
 
-template <bool FILTER, bool IDS, bool VEC>
-__global__ void __launch_bounds__(TPB) k2_classify(Bufs B) {
+template <bool FILTER, bool IDS>
+__global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TileRing<STREAM_T, STREAM_NS, IDS> R;
+  R.carve(smem_raw);
   Ctl* c = B.ctl;
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -311,78 +347,97 @@ __global__ void __launch_bounds__(TPB) k2_classify(Bufs B) {
     Q[k].ex = c->edges[k][2];
     Q[k].ey = c->edges[k][3];
   }
-  const uint32_t nchunks = (n + 63) >> 6;
-  const uint32_t nw = gridDim.x * WARPS;
   Cand a0 = empty_cand(), a1 = empty_cand();
   uint32_t kept = 0;
   bool noncol = false;
+  if (threadIdx.x == 0) R.init();
+  __syncthreads();
 
-  for (uint32_t k0 = blockIdx.x * WARPS + warp; k0 < nchunks; k0 += K2_U * nw) {
-    double2 xv[K2_U], yv[K2_U];
-    uint2 iv[K2_U];
-    uint32_t cidx[K2_U];
+  // With 4 distinct corners, edge q starts at corner q (left, bottom, right,
+  // top) and the chain base lines start at left (P0) and right (Pr), so the
+  // per-point differences p - corner are shared by the 6 cross products:
+  // the same RN operations as cross() (geometry.hpp:17-19), computed once.
+  const bool quad4 = filt && ne == 4 && c->distinct == 4;
+  const double cxL = c->ext_x[0], cyL = c->ext_y[0], cxB = c->ext_x[1], cyB = c->ext_y[1];
+  const double cxR = c->ext_x[2], cyR = c->ext_y[2], cxT = c->ext_x[3], cyT = c->ext_y[3];
+  auto xprod = [](double ex, double ey, double dx, double dy) {
+    return __dsub_rn(__dmul_rn(ex, dy), __dmul_rn(ey, dx));
+  };
+
+  // one point: returns (keep, lower member, upper member) bits
+  auto visit = [&](double x, double y, uint32_t i, uint32_t id, bool valid) -> uint32_t {
+    const double dxL = __dsub_rn(x, cxL), dyL = __dsub_rn(y, cyL);
+    const double dxR = __dsub_rn(x, cxR), dyR = __dsub_rn(y, cyR);
+    const double cl = xprod(E01.ex, E01.ey, dxL, dyL);  // cross(P0, Pr, p)
+    bool inside = false;
+    if (quad4) {  // hull.cpp:80-90: discard iff cross > 0 for every edge
+      const double dxB = __dsub_rn(x, cxB), dyB = __dsub_rn(y, cyB);
+      const double dxT = __dsub_rn(x, cxT), dyT = __dsub_rn(y, cyT);
+      inside = valid & (xprod(Q[0].ex, Q[0].ey, dxL, dyL) > 0.0) &
+               (xprod(Q[1].ex, Q[1].ey, dxB, dyB) > 0.0) &
+               (xprod(Q[2].ex, Q[2].ey, dxR, dyR) > 0.0) &
+               (xprod(Q[3].ex, Q[3].ey, dxT, dyT) > 0.0);
+    } else if (filt) {  // degenerate quadrilateral (3 distinct corners)
+      inside = valid;
 #pragma unroll
-    for (int u = 0; u < K2_U; ++u) {
-      const uint32_t k = k0 + u * nw;
-      cidx[u] = k < nchunks ? nchunks - 1 - k : NONE;  // backwards over the input
-      xv[u] = yv[u] = make_double2(0.0, 0.0);
-      iv[u] = make_uint2(0u, 0u);
-      if (cidx[u] != NONE) {
-        const uint32_t q = cidx[u] * 32 + lane;  // pair index
-        if (2 * q + 1 < n) {
-          xv[u] = load_pair<VEC>(X, q);
-          yv[u] = load_pair<VEC>(Y, q);
-          if (IDS) iv[u] = load_pair_id<VEC>(I, q);
-        } else if (2 * q < n) {
-          xv[u].x = __ldg(X + 2 * q);
-          yv[u].x = __ldg(Y + 2 * q);
-          if (IDS) iv[u].x = __ldg(I + 2 * q);
+      for (int qq = 0; qq < 4; ++qq)
+        if (qq < ne) inside = inside && (cross_e(Q[qq], x, y) > 0.0);
+    }
+    const bool keep = valid && !inside;
+    noncol = noncol || (valid && cl != 0.0);
+    const bool member = keep && i != p0 && i != pr;
+    const bool lw = member && cl < 0.0;  // hull.cpp:115-117
+    const bool up = member && !(cl < 0.0);
+    if (lw) {
+      cand_visit(a0, -cl, x, y, id, i, true);  // outward_distance(P0, Pr, p)
+    } else if (up) {
+      cand_visit(a1, -xprod(E10.ex, E10.ey, dxR, dyR), x, y, id, i, false);  // outward_distance(Pr, P0, p)
+    }
+    return (uint32_t)keep | ((uint32_t)lw << 1) | ((uint32_t)up << 2);
+  };
+
+  // backwards over the input: K1 just left the tail in L2, K3 starts at the head
+  stream_input(R, n, X, Y, I, nullptr, true, [&](int s, uint32_t first, uint32_t cnt) {
+    const double* xs = R.xs + s * STREAM_T;
+    const double* ys = R.ys + s * STREAM_T;
+    const uint32_t* is = R.is + s * STREAM_T;
+    const uint32_t c4 = cnt & ~3u;
+#pragma unroll
+    for (int k = 0; k < STREAM_T / 64 / SWARPS; ++k) {
+      const uint32_t cc = k * SWARPS + warp;  // chunk of 64 points within the tile
+      if (cc * 64 >= cnt) break;              // warp-uniform
+      const uint32_t j = cc * 64 + 2 * lane;  // this lane's pair
+      double2 xv, yv;
+      uint2 iv = make_uint2(0u, 0u);
+      if (j + 1 < c4) {
+        xv = reinterpret_cast<const double2*>(xs)[j >> 1];
+        yv = reinterpret_cast<const double2*>(ys)[j >> 1];
+        if (IDS) iv = reinterpret_cast<const uint2*>(is)[j >> 1];
+      } else {
+        xv = yv = make_double2(0.0, 0.0);
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t jj = j + h;
+          if (jj < cnt) {
+            const bool sm = jj < c4;
+            (h ? xv.y : xv.x) = sm ? xs[jj] : __ldg(X + first + jj);
+            (h ? yv.y : yv.x) = sm ? ys[jj] : __ldg(Y + first + jj);
+            if (IDS) (h ? iv.y : iv.x) = sm ? is[jj] : __ldg(I + first + jj);
+          }
         }
       }
+      const uint32_t i = first + j;
+      const uint32_t f0 = visit(xv.x, yv.x, i, IDS ? iv.x : i, j < cnt);
+      const uint32_t f1 = visit(xv.y, yv.y, i + 1, IDS ? iv.y : i + 1, j + 1 < cnt);
+      const uint32_t le = __ballot_sync(FULL, f0 & 2u), lodd = __ballot_sync(FULL, f1 & 2u);
+      const uint32_t ue = __ballot_sync(FULL, f0 & 4u), uodd = __ballot_sync(FULL, f1 & 4u);
+      kept += (f0 & 1u) + (f1 & 1u);
+      if (lane == 0) B.bits[(first >> 6) + cc] = make_uint4(le, lodd, ue, uodd);
     }
-#pragma unroll
-    for (int u = 0; u < K2_U; ++u) {
-      if (cidx[u] == NONE) continue;  // warp-uniform
-      uint32_t lo2 = 0, up2 = 0, kp2 = 0;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t i = cidx[u] * 64 + 2 * lane + h;
-        const bool valid = i < n;
-        const double x = h ? xv[u].y : xv[u].x;
-        const double y = h ? yv[u].y : yv[u].x;
-        const double cl = cross_e(E01, x, y);
-        bool inside = false;
-        if (filt) {  // hull.cpp:80-90: discard iff cross > 0 for every edge
-          inside = valid;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq)
-            if (qq < ne) inside = inside && (cross_e(Q[qq], x, y) > 0.0);
-        }
-        const bool keep = valid && !inside;
-        noncol = noncol || (valid && cl != 0.0);
-        const bool member = keep && i != p0 && i != pr;
-        const bool lw = member && cl < 0.0;  // hull.cpp:115-117
-        const bool up = member && !(cl < 0.0);
-        lo2 |= (uint32_t)lw << h;
-        up2 |= (uint32_t)up << h;
-        kp2 |= (uint32_t)keep << h;
-        const uint32_t id = IDS ? (h ? iv[u].y : iv[u].x) : i;
-        if (lw) {
-          cand_visit(a0, -cl, x, y, id, i, true);  // outward_distance(P0, Pr, p)
-        } else if (up) {
-          cand_visit(a1, outward_e(E10, x, y), x, y, id, i, false);  // outward_distance(Pr, P0, p)
-        }
-      }
-      const uint32_t le = __ballot_sync(FULL, lo2 & 1u), lodd = __ballot_sync(FULL, lo2 & 2u);
-      const uint32_t ue = __ballot_sync(FULL, up2 & 1u), uodd = __ballot_sync(FULL, up2 & 2u);
-      kept += __popc(kp2);
-      if (lane == 0) B.bits[cidx[u]] = make_uint4(le, lodd, ue, uodd);
-    }
-  }
+  });
 
   // block reduction of the two chains' farthest candidates
-  __shared__ Cand s_a[2][WARPS];
-  __shared__ uint32_t s_kept[WARPS];
+  __shared__ Cand s_a[2][SWARPS];
+  __shared__ uint32_t s_kept[SWARPS];
   __shared__ int s_last;
   a0 = warp_best(a0, true);
   a1 = warp_best(a1, false);
@@ -396,22 +451,21 @@ __global__ void __launch_bounds__(TPB) k2_classify(Bufs B) {
   }
   __syncthreads();
   if (warp == 0) {
-    a0 = lane < WARPS ? s_a[0][lane] : empty_cand();
-    a1 = lane < WARPS ? s_a[1][lane] : empty_cand();
+    a0 = lane < SWARPS ? s_a[0][lane] : empty_cand();
+    a1 = lane < SWARPS ? s_a[1][lane] : empty_cand();
     a0 = warp_best(a0, true);
     a1 = warp_best(a1, false);
     if (lane == 0) {
       unsigned long long kb = 0;
       bool nc = false;
-      for (int w = 0; w < WARPS; ++w) {
+      for (int w = 0; w < SWARPS; ++w) {
         kb += s_kept[w] & 0x7FFFFFFFu;
         nc = nc || (s_kept[w] >> 31);
       }
       if (kb) atomicAdd(&c->kept, kb);
       if (nc) atomicOr(&c->noncollinear, 1u);
-      const LoadSoA ld{X, Y, I};
-      if (a0.d > 0.0) slot_offer(&B.Sd[0][0], &B.Sw[0][0], a0, true, E01, ld);
-      if (a1.d > 0.0) slot_offer(&B.Sd[0][1], &B.Sw[0][1], a1, false, E10, ld);
+      if (a0.d > 0.0) rec_offer(&B.Sd[0][0], &B.Srec[0][0], a0, true);
+      if (a1.d > 0.0) rec_offer(&B.Sd[0][1], &B.Srec[0][1], a1, false);
       __threadfence();
       s_last = atomicAdd(&c->ticket, 1u) == gridDim.x - 1;
     }
@@ -421,11 +475,7 @@ __global__ void __launch_bounds__(TPB) k2_classify(Bufs B) {
   __threadfence();
   c->ticket = 0;
   // round-1 farthest slots (round 1 offers into Slot[1]; its table has <= 4 entries)
-  for (int t = 0; t < 4; ++t) {
-    B.Sd[1][t] = 0ull;
-    B.Sw[1][t] = NONE;
-  }
-  c->out_cnt[1] = 0;
+  for (int t = 0; t < 4; ++t) rec_clear(&B.Sd[1][t], &B.Srec[1][t]);
   if (!*(volatile uint32_t*)&c->noncollinear) {
     c->status = ST_COLLINEAR;  // hull.cpp:238-248
   } else {
@@ -450,42 +500,36 @@ __global__ void __launch_bounds__(TPB) k2_classify(Bufs B) {
 // host-side launch wrappers
 // ===========================================================================
 
-void launch_k1(const Bufs& B, bool ids, bool vec, int grid, cudaStream_t s) {
-  if (ids) {
-    if (vec) k1_extremes<true, true><<<grid, TPB, 0, s>>>(B);
-    else k1_extremes<true, false><<<grid, TPB, 0, s>>>(B);
+size_t stream_smem_bytes(bool ids) { return ids ? RingI::kBytes : Ring::kBytes; }
+
+cudaError_t configure_stream_kernels_pre() {
+  cudaError_t e;
+  e = cudaFuncSetAttribute(k1_extremes<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring::kBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k1_extremes<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RingI::kBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k2_classify<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring::kBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k2_classify<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring::kBytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k2_classify<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RingI::kBytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k2_classify<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RingI::kBytes);
+}
+
+void launch_k1(const Bufs& B, bool ids, int grid, cudaStream_t s) {
+  if (ids) k1_extremes<true><<<grid, STPB, RingI::kBytes, s>>>(B);
+  else k1_extremes<false><<<grid, STPB, Ring::kBytes, s>>>(B);
+}
+
+void launch_k2(const Bufs& B, bool filter, bool ids, int grid, cudaStream_t s) {
+  if (filter) {
+    if (ids) k2_classify<true, true><<<grid, STPB, RingI::kBytes, s>>>(B);
+    else k2_classify<true, false><<<grid, STPB, Ring::kBytes, s>>>(B);
   } else {
-    if (vec) k1_extremes<false, true><<<grid, TPB, 0, s>>>(B);
-    else k1_extremes<false, false><<<grid, TPB, 0, s>>>(B);
+    if (ids) k2_classify<false, true><<<grid, STPB, RingI::kBytes, s>>>(B);
+    else k2_classify<false, false><<<grid, STPB, Ring::kBytes, s>>>(B);
   }
-}
-
-template <bool FILTER>
-static void launch_k2_t(const Bufs& B, bool ids, bool vec, int grid, cudaStream_t s) {
-  if (ids) {
-    if (vec) k2_classify<FILTER, true, true><<<grid, TPB, 0, s>>>(B);
-    else k2_classify<FILTER, true, false><<<grid, TPB, 0, s>>>(B);
-  } else {
-    if (vec) k2_classify<FILTER, false, true><<<grid, TPB, 0, s>>>(B);
-    else k2_classify<FILTER, false, false><<<grid, TPB, 0, s>>>(B);
-  }
-}
-
-int k1_blocks_per_sm() {
-  int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_extremes<false, true>, TPB, 0);
-  return b < 1 ? 1 : b;
-}
-
-int k2_blocks_per_sm() {
-  int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k2_classify<true, false, true>, TPB, 0);
-  return b < 1 ? 1 : b;
-}
-
-void launch_k2(const Bufs& B, bool filter, bool ids, bool vec, int grid, cudaStream_t s) {
-  if (filter) launch_k2_t<true>(B, ids, vec, grid, s);
-  else launch_k2_t<false>(B, ids, vec, grid, s);
 }
 
 }  // namespace shb

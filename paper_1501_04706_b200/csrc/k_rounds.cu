@@ -39,33 +39,31 @@ SH_DEV Route ldcg_route(const Route* p) {
   return r;
 }
 
-// Route one member (x, y, id) of old segment r:
+// Route one member (x, y, id) of old segment r,
+// branch-free:
 //   left = lower ? lex(p) < lex(C) : lex(C) < lex(p)
-//   d    = outward_distance(left ? (A, C) : (C, B), p); keep iff d > 0
-// Returns false when the member is dropped outright (segment not splittable,
-// or p is C itself).
+//   d    = outward_distance(left ? (A, C) : (C, B), p)   (geometry.hpp:25-27)
+//   keep iff the segment splits, p is not C itself and d > 0 (hull.cpp:199)
 SH_DEV bool route_point(const Route& r, double x, double y, uint32_t id, double& d,
-                        uint32_t& nseg, bool& left) {
-  if (!(r.flags & RT_SPLIT) || id == r.cid) return false;
+                        uint32_t& nseg) {
   const bool lower = r.flags & RT_LOWER;
-  left = lower ? lex_less(x, y, r.cx, r.cy) : lex_less(r.cx, r.cy, x, y);
-  const Edge e = left ? make_edge(r.ax, r.ay, r.cx, r.cy) : make_edge(r.cx, r.cy, r.bx, r.by);
-  d = outward_e(e, x, y);
+  const double ux = lower ? x : r.cx, uy = lower ? y : r.cy;
+  const double vx = lower ? r.cx : x, vy = lower ? r.cy : y;
+  const bool left = lex_less(ux, uy, vx, vy);
+  const double ax = left ? r.ax : r.cx, ay = left ? r.ay : r.cy;
+  const double bx = left ? r.cx : r.bx, by = left ? r.cy : r.by;
+  d = outward_e(make_edge(ax, ay, bx, by), x, y);
   nseg = r.ns + (left ? 0u : 1u);
-  return d > 0.0;  // hull.cpp:199 keep iff d > 0 (heads are not members)
+  return (r.flags & RT_SPLIT) && id != r.cid && d > 0.0;
 }
 
-SH_DEV Edge route_edge(const Route& r, bool left) {
-  return left ? make_edge(r.ax, r.ay, r.cx, r.cy) : make_edge(r.cx, r.cy, r.bx, r.by);
-}
-
-// Block-contiguous output reservation for one tile.  keepm bit j says point
-// j of this thread survives; positions are written to pos[j].  Contains two
-// __syncthreads.  One atomicAdd per tile on the round's survivor counter.
-template <int NP, int NW>
-SH_DEV void reserve_tile(uint32_t keepm, uint32_t (&pos)[NP], uint32_t* counter,
-                         uint32_t* s_wcnt) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Dense append of this thread's survivors to the CTA's run of the next live
+// set: one shared-memory atomicAdd per warp, no global atomics, no barrier.
+template <int NP>
+SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py)[NP],
+                       const uint32_t (&pid)[NP], const uint32_t (&pseg)[NP], uint32_t* s_off,
+                       double2* Oxy, uint2* Ois, uint32_t base) {
+  const int lane = threadIdx.x & 31;
   uint32_t bal[NP];
   uint32_t tot = 0;
 #pragma unroll
@@ -73,90 +71,129 @@ SH_DEV void reserve_tile(uint32_t keepm, uint32_t (&pos)[NP], uint32_t* counter,
     bal[j] = __ballot_sync(FULL, (keepm >> j) & 1u);
     tot += __popc(bal[j]);
   }
-  if (lane == 0) s_wcnt[warp] = tot;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t v = lane < NW ? s_wcnt[lane] : 0u;
-    uint32_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const uint32_t all = __shfl_sync(FULL, incl, 31);
-    uint32_t base = 0;
-    if (lane == 0 && all) base = atomicAdd(counter, all);
-    base = __shfl_sync(FULL, base, 0);
-    if (lane < NW) s_wcnt[lane] = base + incl - v;
-  }
-  __syncthreads();
-  uint32_t off = s_wcnt[warp];
+  if (tot == 0) return;  // warp-uniform
+  uint32_t off = 0;
+  if (lane == 0) off = atomicAdd(s_off, tot);
+  off = base + __shfl_sync(FULL, off, 0);
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
-    pos[j] = off + __popc(bal[j] & lt);
+    if ((keepm >> j) & 1u) {
+      const uint32_t e = off + __popc(bal[j] & lt);
+      Oxy[e] = make_double2(px[j], py[j]);
+      Ois[e] = make_uint2(pid[j], pseg[j]);
+    }
     off += __popc(bal[j]);
   }
 }
 
-// Shared-memory farthest slots of one CTA (small next tables).
-//   phase A (per kept point): atomicMax on the distance bits
-//   __syncthreads (all of the tile's rows are now visible block-wide)
-//   phase B (points at the block maximum): CAS on the winner with the full
-//   comparator, incumbent read back from the live set
-// then, once per round, flush_slots() offers each CTA record to the global slot.
-template <int NP, class EdgeOf>
-SH_DEV void offer_tile_smem(unsigned long long* s_db, uint32_t* s_win, uint32_t keepm,
-                            const double (&px)[NP], const double (&py)[NP],
-                            const double (&pd)[NP], const uint32_t (&pid)[NP],
-                            const uint32_t (&pseg)[NP], const uint32_t (&pos)[NP],
-                            const EdgeOf& edge_of, uint32_t lowmask, const LoadLive& ld) {
-  uint32_t candm = 0;
+// Farthest-point contenders of a CTA with shared-memory slots (small tables).
+//   phase A (tile k): filter on the running maximum, atomicMax on the slot's
+//     distance bits; points that reached the maximum are listed in list k%3
+//   phase B (tile k+1, after the end-of-tile barrier): listed points still at
+//     the slot maximum update the slot record under its lock
+// Lists are triple-buffered so the reset of list (k+1)%3 in tile k never
+// races with a reader or a writer.
+struct CEntry {
+  double d, x, y;
+  uint32_t id, tl;  // tl = slot << 1 | lower
+};
+struct CList {
+  CEntry e[3][CLIST];
+  uint32_t n[3];
+};
+
+template <int NP>
+SH_DEV void contend_tile(unsigned long long* s_db, SlotRec* s_rec, CList& L, uint32_t k,
+                         uint32_t keepm, const double (&px)[NP], const double (&py)[NP],
+                         const double (&pd)[NP], const uint32_t (&pid)[NP],
+                         const uint32_t (&pseg)[NP], uint32_t lowm) {
+  const uint32_t b = k % 3u;
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
     if ((keepm >> j) & 1u) {
       const unsigned long long db = (unsigned long long)__double_as_longlong(pd[j]);
       if (db >= *(volatile unsigned long long*)&s_db[pseg[j]]) {
         const unsigned long long old = atomicMax(&s_db[pseg[j]], db);
-        if (db >= old) candm |= 1u << j;
+        if (db >= old) {
+          const uint32_t i = atomicAdd(&L.n[b], 1u);
+          if (i < (uint32_t)CLIST) {
+            CEntry ce;
+            ce.d = pd[j]; ce.x = px[j]; ce.y = py[j]; ce.id = pid[j];
+            ce.tl = (pseg[j] << 1) | ((lowm >> j) & 1u);
+            L.e[b][i] = ce;
+          } else {  // list overflow (adversarial order): resolve right away
+            Cand me;
+            me.d = pd[j]; me.x = px[j]; me.y = py[j]; me.id = pid[j]; me.pos = 0;
+            rec_update<true>(&s_rec[pseg[j]], me, (lowm >> j) & 1u);
+          }
+        }
       }
     }
   }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < NP; ++j) {
-    if ((candm >> j) & 1u) {
-      const unsigned long long db = (unsigned long long)__double_as_longlong(pd[j]);
-      if (db == *(volatile unsigned long long*)&s_db[pseg[j]]) {
-        Cand me;
-        me.d = pd[j]; me.x = px[j]; me.y = py[j]; me.id = pid[j]; me.pos = pos[j];
-        slot_offer(&s_db[pseg[j]], &s_win[pseg[j]], me, (lowmask >> j) & 1u, edge_of(j), ld);
-      }
+}
+
+SH_DEV void resolve_list(unsigned long long* s_db, SlotRec* s_rec, CList& L, uint32_t b) {
+  const uint32_t cnt = min(*(volatile uint32_t*)&L.n[b], (uint32_t)CLIST);
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const CEntry ce = L.e[b][i];
+    const uint32_t t = ce.tl >> 1;
+    if ((unsigned long long)__double_as_longlong(ce.d) == *(volatile unsigned long long*)&s_db[t]) {
+      Cand me;
+      me.d = ce.d; me.x = ce.x; me.y = ce.y; me.id = ce.id; me.pos = 0;
+      rec_update<true>(&s_rec[t], me, ce.tl & 1u);
     }
   }
+}
+
+// CTA records -> global records of the next round's farthest points
+SH_DEV void flush_slots(const unsigned long long* s_db, const SlotRec* s_rec, uint32_t Sn,
+                        uint32_t Slon, unsigned long long* Sd, SlotRec* Srec) {
+  for (uint32_t t = threadIdx.x; t < Sn; t += blockDim.x) {
+    const volatile SlotRec* r = s_rec + t;
+    if (r->id != NONE) {
+      Cand me;
+      me.d = r->d; me.x = r->x; me.y = r->y; me.id = r->id; me.pos = 0;
+      rec_offer(Sd + t, Srec + t, me, t < Slon);
+    }
+  }
+}
+
+// sum of nruns run counts, computed by the whole CTA (contains barriers)
+SH_DEV uint32_t sum_runs(const uint32_t* cnt, uint32_t nruns, uint32_t* s_ws) {
+  uint32_t v = 0;
+  for (uint32_t j = threadIdx.x; j < nruns; j += blockDim.x) v += __ldcg(cnt + j);
+  uint32_t tot;
+  block_exclusive_scan(v, s_ws, &tot);
+  return tot;
 }
 
 // ===========================================================================
 // K3: round 1 straight from the input
 // ===========================================================================
 
-constexpr int K3_U = 4;                   // 64-point chunks per warp per tile
-constexpr int K3_NP = 2 * K3_U;           // points per thread per tile
-constexpr int K3_CHUNKS = WARPS * K3_U;   // chunks per tile (2048 points)
+constexpr int K3_NS = STREAM_NS;
+constexpr int K3_NP = 2 * (STREAM_T / 64 / SWARPS);   // points per thread per tile
 
-template <bool VEC>
-SH_DEV double2 ldcs_pair(const double* __restrict__ a, uint32_t q) {
-  if (VEC) return __ldcs(reinterpret_cast<const double2*>(a) + q);
-  return make_double2(__ldcs(a + 2 * q), __ldcs(a + 2 * q + 1));
-}
+template <bool IDS>
+struct K3Layout {
+  using Ring = TileRing<STREAM_T, K3_NS, IDS, 16>;
+  static constexpr size_t kRing = (Ring::kBytes + 127) / 128 * 128;
+  static constexpr size_t kBytes = kRing + sizeof(CList);
+};
 
-template <bool IDS, bool VEC>
-__global__ void __launch_bounds__(TPB) k3_round1(Bufs B) {
+template <bool IDS>
+__global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  using L = K3Layout<IDS>;
+  typename L::Ring R;
+  R.carve(smem_raw);
+  CList& cl = *reinterpret_cast<CList*>(smem_raw + L::kRing);
   __shared__ Route s_rt[2];
   __shared__ unsigned long long s_db[4];
-  __shared__ uint32_t s_win[4], s_from[4];
-  __shared__ uint32_t s_wcnt[WARPS];
-  __shared__ uint32_t s_Sn, s_Slon;
+  __shared__ SlotRec s_rec[4];
+  __shared__ uint32_t s_off, s_Sn, s_Slon;
+  __shared__ uint32_t s_ws[SWARPS + 1];
   __shared__ int s_last;
   Ctl* c = B.ctl;
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
@@ -165,36 +202,32 @@ __global__ void __launch_bounds__(TPB) k3_round1(Bufs B) {
   const double* __restrict__ X = B.in_x;
   const double* __restrict__ Y = B.in_y;
   const uint32_t* __restrict__ I = B.in_id;
-  double2* Oxy = B.Lxy[1];
-  uint2* Ois = B.Lis[1];
 
   // ---- table phase (S = 2: the lower chain P0->Pr and the upper chain Pr->P0) ----
   if (threadIdx.x == 0) {
+    R.init();
     uint32_t ns = 0, Slon = 1;
     for (int s = 0; s < 2; ++s) {
-      const uint32_t w = __ldcg(B.Sw[0] + s);
-      const bool split = w != NONE;
+      const SlotRec* cr = B.Srec[0] + s;
+      const uint32_t cid = __ldcg(&cr->id);
+      const bool split = cid != NONE;
       Route r;
       r.ax = __ldcg(B.Tx[0] + s);
       r.ay = __ldcg(B.Ty[0] + s);
       r.bx = __ldcg(B.Tx[0] + (s ^ 1));
       r.by = __ldcg(B.Ty[0] + (s ^ 1));
-      r.cx = split ? __ldcg(X + w) : 0.0;
-      r.cy = split ? __ldcg(Y + w) : 0.0;
-      r.cid = split ? (I ? __ldcg(I + w) : w) : NONE;
+      r.cx = split ? __ldcg(&cr->x) : 0.0;
+      r.cy = split ? __ldcg(&cr->y) : 0.0;
+      r.cid = cid;
       r.ns = ns;
       r.flags = (split ? RT_SPLIT : 0u) | (s == 0 ? RT_LOWER : 0u);
       r.pad = 0;
       s_rt[s] = r;
-      s_from[ns] = s;
       if (blockIdx.x == 0) {
         B.Tx[1][ns] = r.ax;
         B.Ty[1][ns] = r.ay;
         B.Tid[1][ns] = __ldcg(B.Tid[0] + s);
-      }
-      if (split) {
-        s_from[ns + 1] = s | 0x80000000u;
-        if (blockIdx.x == 0) {
+        if (split) {
           B.Tx[1][ns + 1] = r.cx;
           B.Ty[1][ns + 1] = r.cy;
           B.Tid[1][ns + 1] = r.cid;
@@ -205,127 +238,105 @@ __global__ void __launch_bounds__(TPB) k3_round1(Bufs B) {
     }
     s_Sn = ns;
     s_Slon = Slon;
-    for (int t = 0; t < 4; ++t) {
-      s_db[t] = 0ull;
-      s_win[t] = NONE;
-    }
-    if (blockIdx.x == 0) {  // clear round 2's slots and counter
-      for (int t = 0; t < 8; ++t) {
-        B.Sd[2][t] = 0ull;
-        B.Sw[2][t] = NONE;
-      }
-      c->out_cnt[2] = 0;
-    }
+    s_off = 0;
+    for (int t = 0; t < 4; ++t) rec_clear(&s_db[t], &s_rec[t]);
+    for (int b = 0; b < 3; ++b) cl.n[b] = 0;
+    if (blockIdx.x == 0)  // clear round 2's slots
+      for (int t = 0; t < 8; ++t) rec_clear(&B.Sd[2][t], &B.Srec[2][t]);
   }
   __syncthreads();
   const Route rlo = s_rt[0], rup = s_rt[1];
   const uint32_t Sn = s_Sn, Slon = s_Slon;
-  const LoadLive ld{Oxy, Ois};
+  const uint32_t run_base = blockIdx.x * B.run_q;
+  double2* Oxy = B.Lxy[1];
+  uint2* Ois = B.Lis[1];
+  uint32_t k = 0;
 
-  // ---- point phase ----
-  const uint32_t nchunks = (n + 63) >> 6;
-  const uint32_t ntiles = (nchunks + K3_CHUNKS - 1) / K3_CHUNKS;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // ---- point phase: forward over the input (K2 left the head in L2) ----
+  stream_input(R, n, X, Y, I, reinterpret_cast<const unsigned char*>(B.bits), false,
+               [&](int s, uint32_t first, uint32_t cnt) {
+    if (k) resolve_list(s_db, s_rec, cl, (k - 1) % 3u);
+    if (threadIdx.x == 0) cl.n[(k + 1) % 3u] = 0;
+    const double* xs = R.xs + s * STREAM_T;
+    const double* ys = R.ys + s * STREAM_T;
+    const uint32_t* is = R.is + s * STREAM_T;
+    const uint4* bs = reinterpret_cast<const uint4*>(R.aux + s * L::Ring::kAuxBytes);
+    const uint32_t c4 = cnt & ~3u;
     double px[K3_NP], py[K3_NP], pd[K3_NP];
-    uint32_t pid[K3_NP], pseg[K3_NP], pos[K3_NP];
-    uint32_t keepm = 0, lowm = 0, leftm = 0;
-    uint4 bits[K3_U];
+    uint32_t pid[K3_NP], pseg[K3_NP];
+    uint32_t keepm = 0, lowm = 0;
 #pragma unroll
-    for (int u = 0; u < K3_U; ++u) {
-      const uint32_t ch = tile * K3_CHUNKS + u * WARPS + warp;
-      bits[u] = make_uint4(0u, 0u, 0u, 0u);
+    for (int kk = 0; kk < K3_NP / 2; ++kk) {
+      const uint32_t cc = kk * SWARPS + warp;  // chunk of 64 points within the tile
+      const uint32_t j = cc * 64 + 2 * lane;
+      uint4 bits = make_uint4(0u, 0u, 0u, 0u);
       double2 xv = make_double2(0.0, 0.0), yv = xv;
-      if (ch < nchunks) {
-        bits[u] = __ldg(B.bits + ch);
-        const uint32_t q = ch * 32 + lane;
-        if (2 * q + 1 < n) {
-          xv = ldcs_pair<VEC>(X, q);
-          yv = ldcs_pair<VEC>(Y, q);
-        } else if (2 * q < n) {
-          xv.x = __ldcs(X + 2 * q);
-          yv.x = __ldcs(Y + 2 * q);
-        }
-      }
-      px[2 * u] = xv.x; px[2 * u + 1] = xv.y;
-      py[2 * u] = yv.x; py[2 * u + 1] = yv.y;
-    }
-#pragma unroll
-    for (int u = 0; u < K3_U; ++u) {
-      const uint32_t ch = tile * K3_CHUNKS + u * WARPS + warp;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = 2 * u + h;
-        const uint32_t lw = ((h ? bits[u].y : bits[u].x) >> lane) & 1u;
-        const uint32_t uw = ((h ? bits[u].w : bits[u].z) >> lane) & 1u;
-        pd[j] = 0.0;
-        pseg[j] = 0;
-        const uint32_t i = ch * 64 + 2 * lane + h;
-        pid[j] = 0;
-        if (lw | uw) {
-          pid[j] = IDS ? __ldg(I + i) : i;
-          const Route& r = lw ? rlo : rup;
-          bool left = false;
-          if (route_point(r, px[j], py[j], pid[j], pd[j], pseg[j], left)) {
-            keepm |= 1u << j;
-            if (left) leftm |= 1u << j;
-            if (lw) lowm |= 1u << j;
+      uint2 iv = make_uint2(0u, 0u);
+      if (cc * 64 < cnt) {
+        bits = bs[cc];
+        if (j + 1 < c4) {
+          xv = reinterpret_cast<const double2*>(xs)[j >> 1];
+          yv = reinterpret_cast<const double2*>(ys)[j >> 1];
+          if (IDS) iv = reinterpret_cast<const uint2*>(is)[j >> 1];
+        } else {
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t jj = j + h;
+            if (jj < cnt) {
+              const bool sm = jj < c4;
+              (h ? xv.y : xv.x) = sm ? xs[jj] : __ldg(X + first + jj);
+              (h ? yv.y : yv.x) = sm ? ys[jj] : __ldg(Y + first + jj);
+              if (IDS) (h ? iv.y : iv.x) = sm ? is[jj] : __ldg(I + first + jj);
+            }
           }
         }
       }
-    }
-    reserve_tile<K3_NP, WARPS>(keepm, pos, &c->out_cnt[1], s_wcnt);
 #pragma unroll
-    for (int j = 0; j < K3_NP; ++j) {
-      if ((keepm >> j) & 1u) {
-        Oxy[pos[j]] = make_double2(px[j], py[j]);
-        Ois[pos[j]] = make_uint2(pid[j], pseg[j]);
+      for (int h = 0; h < 2; ++h) {
+        const int q = 2 * kk + h;
+        px[q] = h ? xv.y : xv.x;
+        py[q] = h ? yv.y : yv.x;
+        pid[q] = IDS ? (h ? iv.y : iv.x) : first + j + h;
+        const uint32_t lw = ((h ? bits.y : bits.x) >> lane) & 1u;
+        const uint32_t uw = ((h ? bits.w : bits.z) >> lane) & 1u;
+        const bool keep = route_point(lw ? rlo : rup, px[q], py[q], pid[q], pd[q], pseg[q]);
+        if ((lw | uw) && keep) keepm |= 1u << q;
+        if (lw) lowm |= 1u << q;
       }
     }
-    offer_tile_smem<K3_NP>(s_db, s_win, keepm, px, py, pd, pid, pseg, pos,
-                           [&](int j) {
-                             return route_edge(((lowm >> j) & 1u) ? rlo : rup, (leftm >> j) & 1u);
-                           },
-                           lowm, ld);
-  }
+    contend_tile<K3_NP>(s_db, s_rec, cl, k, keepm, px, py, pd, pid, pseg, lowm);
+    run_append<K3_NP>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, run_base);
+    ++k;
+  });
+  if (k) resolve_list(s_db, s_rec, cl, (k - 1) % 3u);
 
-  // ---- flush the CTA's slots to the global slots of round 2's argmax ----
+  // ---- flush the CTA's records to the global slots of round 2's argmax ----
   __syncthreads();
-  __threadfence();
-  if (threadIdx.x < Sn) {
-    const uint32_t t = threadIdx.x;
-    const uint32_t w = s_win[t];
-    if (w != NONE) {
-      Cand me;
-      ld(w, me.x, me.y, me.id);
-      me.d = __longlong_as_double((long long)s_db[t]);
-      me.pos = w;
-      const uint32_t f = s_from[t];
-      const Route& r = s_rt[f & 1u];
-      slot_offer(B.Sd[1] + t, B.Sw[1] + t, me, t < Slon, route_edge(r, (f >> 31) == 0u),
-                 ld);
-    }
-  }
+  flush_slots(s_db, s_rec, Sn, Slon, B.Sd[1], B.Srec[1]);
+  if (threadIdx.x == 0) B.run_cnt[1][blockIdx.x] = s_off;
 
   // ---- last CTA closes round 1 ----
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&c->ticket, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
+  if (!s_last) return;
   __threadfence();
+  const uint32_t mn = sum_runs(B.run_cnt[1], gridDim.x, s_ws);
+  if (threadIdx.x != 0) return;
   c->ticket = 0;
-  const uint32_t mn = *(volatile uint32_t*)&c->out_cnt[1];
   const uint32_t before = c->S_cur + c->m_cur;
   StatRec st;
   st.segments = Sn;
   st.points_remaining = Sn + mn;
   st.points_removed = before - (Sn + mn);
   st.pad = 0;
+  st.end_ns = globaltimer_ns() - *(volatile unsigned long long*)&c->t0_ns;
   B.stats[0] = st;
   c->round = 1;
   c->S_cur = Sn;
   c->Slo_cur = Slon;
   c->m_cur = mn;
+  c->nruns = gridDim.x;
   if (mn == 0) c->status = ST_DONE;
   __threadfence();
 }
@@ -339,10 +350,10 @@ constexpr int KR_U = 4;                // live points per thread per tile
 constexpr int KR_TILE = RTPB * KR_U;   // 2048
 
 struct RoundSmem {
-  Route rt[SMALL_S];               // route entries of a small table   64 KB
-  unsigned long long db[NSLOT];    // CTA farthest slots: distance bits 16 KB
-  uint32_t win[NSLOT];             //                     winner pos     8 KB
-  uint32_t from[NSLOT];            // new segment -> (old segment, side) 8 KB
+  Route rt[SMALL_S];               // route entries of a small table     64 KB
+  unsigned long long db[NSLOT];    // CTA farthest slots: distance bits   16 KB
+  SlotRec rec[NSLOT];              //                     records         64 KB
+  CList cl;                        // phase-B contender lists             24 KB
 };
 
 // Barrier over the CTAs still working on the rounds.
@@ -351,68 +362,60 @@ SH_DEV void rounds_barrier(Ctl* c, uint32_t P) {
   else __syncthreads();
 }
 
+// Route entry of old segment s from head table `pin` and farthest record `cr`.
+SH_DEV Route make_route(const Bufs& B, uint32_t pin, const SlotRec* cr, uint32_t s, uint32_t S,
+                        uint32_t Slo, uint32_t ns) {
+  const uint32_t cid = __ldcg(&cr->id);
+  const bool split = cid != NONE;
+  const uint32_t sb = s + 1 == S ? 0u : s + 1;
+  Route r;
+  r.ax = __ldcg(B.Tx[pin] + s);
+  r.ay = __ldcg(B.Ty[pin] + s);
+  r.bx = __ldcg(B.Tx[pin] + sb);
+  r.by = __ldcg(B.Ty[pin] + sb);
+  r.cx = split ? __ldcg(&cr->x) : 0.0;
+  r.cy = split ? __ldcg(&cr->y) : 0.0;
+  r.cid = cid;
+  r.ns = ns;
+  r.flags = (split ? RT_SPLIT : 0u) | (s < Slo ? RT_LOWER : 0u);
+  r.pad = 0;
+  return r;
+}
+
+SH_DEV void write_heads(const Bufs& B, uint32_t pin, uint32_t pout, const Route& r, uint32_t s) {
+  B.Tx[pout][r.ns] = r.ax;
+  B.Ty[pout][r.ns] = r.ay;
+  B.Tid[pout][r.ns] = __ldcg(B.Tid[pin] + s);
+  if (r.flags & RT_SPLIT) {
+    B.Tx[pout][r.ns + 1] = r.cx;
+    B.Ty[pout][r.ns + 1] = r.cy;
+    B.Tid[pout][r.ns + 1] = r.cid;
+  }
+}
+
 // Small table (S <= SMALL_S), rebuilt by every participating CTA in smem.
 // CTA 0 also writes the next head table.  Returns S', S'lo.
 SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, uint32_t pin,
                         uint32_t pout, uint32_t sin, uint32_t* s_ws, uint32_t& Sn,
                         uint32_t& Slon) {
-  const double2* Cxy = B.Lxy[pin];
-  const uint2* Cis = B.Lis[pin];
-  const double* Tx = B.Tx[pin];
-  const double* Ty = B.Ty[pin];
-  const uint32_t* Ti = B.Tid[pin];
   const bool heads = blockIdx.x == 0;
   uint32_t running = 0, lower_splits = 0;
   for (uint32_t s0 = 0; s0 < S; s0 += RTPB) {
     const uint32_t s = s0 + threadIdx.x;
-    const uint32_t w = s < S ? __ldcg(B.Sw[sin] + s) : NONE;
-    const uint32_t split = (s < S && w != NONE) ? 1u : 0u;
+    const uint32_t split = (s < S && __ldcg(&B.Srec[sin][s].id) != NONE) ? 1u : 0u;
     uint32_t total;
     const uint32_t pre = block_exclusive_scan(split, s_ws, &total);
     lower_splits += (uint32_t)__syncthreads_count(split && s < Slo);
     if (s < S) {
-      const uint32_t ns = s + running + pre;
-      const uint32_t sb = s + 1 == S ? 0u : s + 1;
-      Route r;
-      r.ax = __ldcg(Tx + s);
-      r.ay = __ldcg(Ty + s);
-      r.bx = __ldcg(Tx + sb);
-      r.by = __ldcg(Ty + sb);
-      r.ns = ns;
-      r.flags = (split ? RT_SPLIT : 0u) | (s < Slo ? RT_LOWER : 0u);
-      r.pad = 0;
-      if (split) {
-        const double2 cv = __ldcg(Cxy + w);
-        r.cx = cv.x;
-        r.cy = cv.y;
-        r.cid = __ldcg(&Cis[w].x);
-      } else {
-        r.cx = 0.0;
-        r.cy = 0.0;
-        r.cid = NONE;
-      }
+      const Route r = make_route(B, pin, B.Srec[sin] + s, s, S, Slo, s + running + pre);
       sm.rt[s] = r;
-      sm.from[ns] = s;
-      if (split) sm.from[ns + 1] = s | 0x80000000u;
-      if (heads) {
-        B.Tx[pout][ns] = r.ax;
-        B.Ty[pout][ns] = r.ay;
-        B.Tid[pout][ns] = __ldcg(Ti + s);
-        if (split) {
-          B.Tx[pout][ns + 1] = r.cx;
-          B.Ty[pout][ns + 1] = r.cy;
-          B.Tid[pout][ns + 1] = r.cid;
-        }
-      }
+      if (heads) write_heads(B, pin, pout, r, s);
     }
     running += total;
   }
   Sn = S + running;
   Slon = Slo + lower_splits;
-  for (uint32_t t = threadIdx.x; t < Sn; t += RTPB) {
-    sm.db[t] = 0ull;
-    sm.win[t] = NONE;
-  }
+  for (uint32_t t = threadIdx.x; t < Sn; t += RTPB) rec_clear(&sm.db[t], &sm.rec[t]);
   __syncthreads();
 }
 
@@ -423,11 +426,11 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
                         uint32_t& Slon) {
   Ctl* c = B.ctl;
   const uint32_t per = (S + P - 1) / P;
-  const uint32_t lo = blockIdx.x * per, hi = min(S, lo + per);
+  const uint32_t lo = min(S, blockIdx.x * per), hi = min(S, lo + per);
   // T1: splittable counts of this CTA's range (total and lower chain)
   uint32_t cnt = 0, cnt_lo = 0;
   for (uint32_t s = lo + threadIdx.x; s < hi; s += RTPB) {
-    const bool split = __ldcg(B.Sw[sin] + s) != NONE;
+    const bool split = __ldcg(&B.Srec[sin][s].id) != NONE;
     cnt += split;
     cnt_lo += split && s < Slo;
   }
@@ -459,48 +462,16 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
     if (blockIdx.x == 0 && threadIdx.x == 0) c->status = ST_OVERFLOW;
     return false;
   }
-  const double2* Cxy = B.Lxy[pin];
-  const uint2* Cis = B.Lis[pin];
-  const double* Tx = B.Tx[pin];
-  const double* Ty = B.Ty[pin];
-  const uint32_t* Ti = B.Tid[pin];
   uint32_t running = pre_all;
   for (uint32_t s0 = lo; s0 < hi; s0 += RTPB) {
     const uint32_t s = s0 + threadIdx.x;
-    const uint32_t w = s < hi ? __ldcg(B.Sw[sin] + s) : NONE;
-    const uint32_t split = (s < hi && w != NONE) ? 1u : 0u;
+    const uint32_t split = (s < hi && __ldcg(&B.Srec[sin][s].id) != NONE) ? 1u : 0u;
     uint32_t total;
     const uint32_t p = block_exclusive_scan(split, s_ws, &total);
     if (s < hi) {
-      const uint32_t ns = s + running + p;
-      const uint32_t sb = s + 1 == S ? 0u : s + 1;
-      Route r;
-      r.ax = __ldcg(Tx + s);
-      r.ay = __ldcg(Ty + s);
-      r.bx = __ldcg(Tx + sb);
-      r.by = __ldcg(Ty + sb);
-      r.ns = ns;
-      r.flags = (split ? RT_SPLIT : 0u) | (s < Slo ? RT_LOWER : 0u);
-      r.pad = 0;
-      if (split) {
-        const double2 cv = __ldcg(Cxy + w);
-        r.cx = cv.x;
-        r.cy = cv.y;
-        r.cid = __ldcg(&Cis[w].x);
-      } else {
-        r.cx = 0.0;
-        r.cy = 0.0;
-        r.cid = NONE;
-      }
+      const Route r = make_route(B, pin, B.Srec[sin] + s, s, S, Slo, s + running + p);
       B.route[s] = r;
-      B.Tx[pout][ns] = r.ax;
-      B.Ty[pout][ns] = r.ay;
-      B.Tid[pout][ns] = __ldcg(Ti + s);
-      if (split) {
-        B.Tx[pout][ns + 1] = r.cx;
-        B.Ty[pout][ns + 1] = r.cy;
-        B.Tid[pout][ns + 1] = r.cid;
-      }
+      write_heads(B, pin, pout, r, s);
     }
     running += total;
   }
@@ -509,17 +480,19 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
 }
 
 __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   RoundSmem& sm = *reinterpret_cast<RoundSmem*>(smem_raw);
   __shared__ uint32_t s_ws[RW + 1];
-  __shared__ uint32_t s_wcnt[RW];
+  __shared__ uint32_t s_off;
+  __shared__ uint32_t s_pref[MAX_RUNS + 1];
   Ctl* c = B.ctl;
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   uint32_t r = *(volatile uint32_t*)&c->round + 1;
   uint32_t S = *(volatile uint32_t*)&c->S_cur;
   uint32_t Slo = *(volatile uint32_t*)&c->Slo_cur;
   uint32_t m = *(volatile uint32_t*)&c->m_cur;
-  const uint32_t n = B.n;
+  uint32_t nruns = *(volatile uint32_t*)&c->nruns;
+  const uint32_t n = B.n, q = B.run_q;
   uint32_t P = gridDim.x;
 
   while (true) {
@@ -536,39 +509,44 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     } else if (!table_large(B, S, Slo, pin, pout, sin, P, s_ws, Sn, Slon)) {
       return;
     }
-    // clear round r+1's farthest slots (at most 2 Sn segments) and counter
+    // clear round r+1's farthest slots (at most 2 Sn segments)
     {
       const uint32_t lim = min(2 * Sn, B.s_cap);
-      for (uint32_t t = blockIdx.x * RTPB + threadIdx.x; t < lim; t += P * RTPB) {
-        B.Sd[sres][t] = 0ull;
-        B.Sw[sres][t] = NONE;
-      }
-      if (blockIdx.x == 0 && threadIdx.x == 0) c->out_cnt[sres] = 0;
+      for (uint32_t t = blockIdx.x * RTPB + threadIdx.x; t < lim; t += P * RTPB)
+        rec_clear(B.Sd[sres] + t, B.Srec[sres] + t);
     }
+    if (threadIdx.x == 0) {
+      s_off = 0;
+      for (int b = 0; b < 3; ++b) sm.cl.n[b] = 0;
+    }
+    __syncthreads();
 
-    // ---- point phase ----
+    // ---- point phase: this CTA's runs of the live set -> its run of the next ----
     const double2* Ixy = B.Lxy[pin];
     const uint2* Iis = B.Lis[pin];
     double2* Oxy = B.Lxy[pout];
     uint2* Ois = B.Lis[pout];
-    const LoadLive ld{Oxy, Ois};
     unsigned long long* Sd = B.Sd[sout];
-    uint32_t* Sw = B.Sw[sout];
-    const uint32_t ntiles = (m + KR_TILE - 1) / KR_TILE;
-    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += P) {
+    SlotRec* Srec = B.Srec[sout];
+    const uint32_t obase = (P == 1 ? 0u : blockIdx.x) * q;
+    uint32_t k = 0;
+    // One tile of live points: element e < cnt of the range `map` resolves.
+    auto do_tile = [&](uint32_t t0, uint32_t cnt, auto map) {
+      if (small && k) resolve_list(sm.db, sm.rec, sm.cl, (k - 1) % 3u);
+      if (small && threadIdx.x == 0) sm.cl.n[(k + 1) % 3u] = 0;
       double px[KR_U], py[KR_U], pd[KR_U];
-      uint32_t pid[KR_U], pseg[KR_U], pos[KR_U];
-      uint32_t keepm = 0, lowm = 0, leftm = 0;
-      uint32_t oseg[KR_U];
+      uint32_t pid[KR_U], pseg[KR_U], oseg[KR_U];
+      uint32_t keepm = 0, lowm = 0;
 #pragma unroll
       for (int u = 0; u < KR_U; ++u) {
-        const uint32_t e = tile * KR_TILE + u * RTPB + threadIdx.x;
+        const uint32_t e = t0 + u * RTPB + threadIdx.x;
         px[u] = py[u] = 0.0;
         pid[u] = 0;
         oseg[u] = NONE;
-        if (e < m) {
-          const double2 v = __ldcs(Ixy + e);
-          const uint2 is = __ldcs(Iis + e);
+        if (e < cnt) {
+          const uint32_t ph = map(e);
+          const double2 v = __ldcg(Ixy + ph);
+          const uint2 is = __ldcg(Iis + ph);
           px[u] = v.x;
           py[u] = v.y;
           pid[u] = is.x;
@@ -581,78 +559,91 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
         pseg[u] = 0;
         if (oseg[u] != NONE) {
           const Route rr = small ? sm.rt[oseg[u]] : ldcg_route(B.route + oseg[u]);
-          bool left = false;
-          if (route_point(rr, px[u], py[u], pid[u], pd[u], pseg[u], left)) {
-            keepm |= 1u << u;
-            if (left) leftm |= 1u << u;
-            if (rr.flags & RT_LOWER) lowm |= 1u << u;
-          }
+          if (route_point(rr, px[u], py[u], pid[u], pd[u], pseg[u])) keepm |= 1u << u;
+          if (rr.flags & RT_LOWER) lowm |= 1u << u;
         }
       }
-      reserve_tile<KR_U, RW>(keepm, pos, &c->out_cnt[sout], s_wcnt);
-#pragma unroll
-      for (int u = 0; u < KR_U; ++u) {
-        if ((keepm >> u) & 1u) {
-          Oxy[pos[u]] = make_double2(px[u], py[u]);
-          Ois[pos[u]] = make_uint2(pid[u], pseg[u]);
-        }
-      }
-      auto edge_of = [&](int u) {
-        const Route rr = small ? sm.rt[oseg[u]] : ldcg_route(B.route + oseg[u]);
-        return route_edge(rr, (leftm >> u) & 1u);
-      };
       if (small) {
-        offer_tile_smem<KR_U>(sm.db, sm.win, keepm, px, py, pd, pid, pseg, pos, edge_of, lowm,
-                              ld);
-      } else if (keepm) {
-        __threadfence();
+        contend_tile<KR_U>(sm.db, sm.rec, sm.cl, k, keepm, px, py, pd, pid, pseg, lowm);
+      } else {
 #pragma unroll
         for (int u = 0; u < KR_U; ++u) {
           if ((keepm >> u) & 1u) {
             Cand me;
-            me.d = pd[u]; me.x = px[u]; me.y = py[u]; me.id = pid[u]; me.pos = pos[u];
-            slot_offer(Sd + pseg[u], Sw + pseg[u], me, (lowm >> u) & 1u, edge_of(u), ld);
+            me.d = pd[u]; me.x = px[u]; me.y = py[u]; me.id = pid[u]; me.pos = 0;
+            rec_offer(Sd + pseg[u], Srec + pseg[u], me, (lowm >> u) & 1u);
           }
         }
       }
-    }
-    if (small) {  // flush the CTA's slots
+      run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase);
       __syncthreads();
-      __threadfence();
-      for (uint32_t t = threadIdx.x; t < Sn; t += RTPB) {
-        const uint32_t w = sm.win[t];
-        if (w != NONE) {
-          Cand me;
-          ld(w, me.x, me.y, me.id);
-          me.d = __longlong_as_double((long long)sm.db[t]);
-          me.pos = w;
-          const uint32_t f = sm.from[t];
-          const Route& rr = sm.rt[f & 0x7FFFFFFFu];
-          slot_offer(Sd + t, Sw + t, me, t < Slon, route_edge(rr, (f >> 31) == 0u), ld);
+      ++k;
+    };
+    if (P == 1 && nruns > 1) {
+      // single CTA over many runs: walk them as one virtual range through an
+      // smem prefix of the run counts (binary search per point)
+      uint32_t* pref = s_pref;
+      uint32_t tot;
+      for (uint32_t j0 = 0; j0 < nruns; j0 += RTPB) {
+        const uint32_t j = j0 + threadIdx.x;
+        const uint32_t v = j < nruns ? __ldcg(B.run_cnt[pin] + j) : 0u;
+        const uint32_t base0 = j0 ? pref[j0] : 0u;
+        const uint32_t ex = block_exclusive_scan(v, s_ws, &tot);
+        if (j < nruns) pref[j] = base0 + ex;
+        if (j0 + RTPB >= nruns && threadIdx.x == 0) pref[nruns] = base0 + tot;
+        __syncthreads();
+        if (j0 + RTPB < nruns && threadIdx.x == 0) pref[j0 + RTPB] = base0 + tot;
+        __syncthreads();
+      }
+      const uint32_t total = pref[nruns];
+      auto map = [&](uint32_t e) {
+        uint32_t lo = 0, hi = nruns;  // pref[lo] <= e < pref[hi]
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (pref[mid] <= e) lo = mid; else hi = mid;
         }
+        return lo * q + (e - pref[lo]);
+      };
+      for (uint32_t t0 = 0; t0 < total; t0 += KR_TILE) do_tile(t0, total, map);
+    } else {
+      for (uint32_t run = blockIdx.x; run < nruns; run += P) {
+        const uint32_t rc = __ldcg(B.run_cnt[pin] + run);
+        const uint32_t ibase = run * q;
+        auto map = [ibase](uint32_t e) { return ibase + e; };
+        for (uint32_t t0 = 0; t0 < rc; t0 += KR_TILE) do_tile(t0, rc, map);
       }
     }
+    if (small) {
+      if (k) resolve_list(sm.db, sm.rec, sm.cl, (k - 1) % 3u);
+      __syncthreads();
+      flush_slots(sm.db, sm.rec, Sn, Slon, Sd, Srec);
+    }
+    const uint32_t nruns_out = P == 1 ? 1u : P;
+    if (threadIdx.x == 0) B.run_cnt[pout][P == 1 ? 0u : blockIdx.x] = s_off;
     rounds_barrier(c, P);
 
     // ---- close round r (every participating CTA computes the same) ----
-    const uint32_t mn = __ldcg(&c->out_cnt[sout]);
+    const uint32_t mn = sum_runs(B.run_cnt[pout], nruns_out, s_ws);
     if (blockIdx.x == 0 && threadIdx.x == 0 && r <= (uint32_t)STATS_CAP) {
       StatRec st;
       st.segments = Sn;
       st.points_remaining = Sn + mn;
       st.points_removed = (S + m) - (Sn + mn);
       st.pad = 0;
+      st.end_ns = globaltimer_ns() - *(volatile unsigned long long*)&c->t0_ns;
       B.stats[r - 1] = st;
     }
     S = Sn;
     Slo = Slon;
     m = mn;
+    nruns = nruns_out;
     if (mn == 0 || r + 1 > n) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         c->round = r;
         c->S_cur = S;
         c->Slo_cur = Slo;
         c->m_cur = m;
+        c->nruns = nruns;
         c->status = mn == 0 ? ST_DONE : ST_INTERNAL;  // hull.cpp:265-267
         __threadfence();
       }
@@ -696,20 +687,19 @@ int rounds_blocks_per_sm() {
   return b < 1 ? 1 : b;
 }
 
-int k3_blocks_per_sm() {
-  int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k3_round1<false, true>, TPB, 0);
-  return b < 1 ? 1 : b;
+cudaError_t configure_stream_kernels_k3() {
+  cudaError_t e = cudaFuncSetAttribute(k3_round1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)K3Layout<false>::kBytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k3_round1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)K3Layout<true>::kBytes);
 }
 
-void launch_k3(const Bufs& B, bool ids, bool vec, int grid, cudaStream_t s) {
-  if (ids) {
-    if (vec) k3_round1<true, true><<<grid, TPB, 0, s>>>(B);
-    else k3_round1<true, false><<<grid, TPB, 0, s>>>(B);
-  } else {
-    if (vec) k3_round1<false, true><<<grid, TPB, 0, s>>>(B);
-    else k3_round1<false, false><<<grid, TPB, 0, s>>>(B);
-  }
+void launch_k3(const Bufs& B, bool ids, int grid, cudaStream_t s) {
+  if (ids)
+    k3_round1<true><<<grid, STPB, K3Layout<true>::kBytes, s>>>(B);
+  else
+    k3_round1<false><<<grid, STPB, K3Layout<false>::kBytes, s>>>(B);
 }
 
 cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s) {

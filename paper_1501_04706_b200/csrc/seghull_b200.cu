@@ -21,9 +21,11 @@
 #include "hull_kernels.cuh"
 
 namespace shb {
-void launch_k1(const Bufs& B, bool ids, bool vec, int grid, cudaStream_t s);
-void launch_k2(const Bufs& B, bool filter, bool ids, bool vec, int grid, cudaStream_t s);
-void launch_k3(const Bufs& B, bool ids, bool vec, int grid, cudaStream_t s);
+void launch_k1(const Bufs& B, bool ids, int grid, cudaStream_t s);
+void launch_k2(const Bufs& B, bool filter, bool ids, int grid, cudaStream_t s);
+void launch_k3(const Bufs& B, bool ids, int grid, cudaStream_t s);
+cudaError_t configure_stream_kernels_pre();
+cudaError_t configure_stream_kernels_k3();
 size_t rounds_smem_bytes();
 cudaError_t configure_round_kernels();
 int rounds_blocks_per_sm();
@@ -37,9 +39,6 @@ void launch_gen_disk(double* x, double* y, unsigned long long n, unsigned long l
                      Ctl* c, unsigned long long* status, uint32_t* epoch, int grid,
                      cudaStream_t s);
 int gen_tile_points();
-int k1_blocks_per_sm();
-int k2_blocks_per_sm();
-int k3_blocks_per_sm();
 }  // namespace shb
 
 using namespace shb;
@@ -61,7 +60,6 @@ struct DeviceInfo {
   int sm_count = 0;
   bool configured = false;
   int rounds_bps = 1;  // co-resident CTAs of the cooperative round kernel per SM
-  int k1_bps = 1, k2_bps = 1, k3_bps = 1;
 };
 
 std::mutex g_mutex;
@@ -81,7 +79,6 @@ struct Workspace {
   cudaEvent_t ev[8] = {};
   size_t tiles_cap = 0;
   int stream_grid = 0, rounds_grid = 0;
-  int grid1 = 0, grid2 = 0, grid3 = 0;  // one full wave of each streaming kernel
 
   ~Workspace() {
     int cur = 0;
@@ -109,9 +106,8 @@ DeviceInfo& device_info(int device) {
     CK(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, device));
     CK(configure_round_kernels());
     d.rounds_bps = rounds_blocks_per_sm();
-    d.k1_bps = k1_blocks_per_sm();
-    d.k2_bps = k2_blocks_per_sm();
-    d.k3_bps = k3_blocks_per_sm();
+    CK(configure_stream_kernels_pre());
+    CK(configure_stream_kernels_k3());
     d.configured = true;
   }
   return d;
@@ -136,10 +132,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   const uint64_t N = std::max<uint64_t>(n_cap, 64), S = std::max<uint64_t>(s_cap, 64);
   // streaming kernels: 4 CTAs of 256 threads per SM; the round kernel: every
   // co-resident CTA (cooperative launch)
-  ws->stream_grid = di.sm_count * 4;
-  ws->grid1 = di.sm_count * di.k1_bps;
-  ws->grid2 = di.sm_count * di.k2_bps;
-  ws->grid3 = di.sm_count * di.k3_bps;
+  ws->stream_grid = di.sm_count;  // K1/K2/K3: one TMA-fed CTA per SM
   ws->rounds_grid = std::min(di.sm_count * di.rounds_bps, MAX_ROUND_BLOCKS);
   ws->tiles_cap = (N + gen_tile_points() - 1) / gen_tile_points() + 64;
 
@@ -152,15 +145,19 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   };
   const size_t o_ctl = take(sizeof(Ctl));
   const size_t o_epoch = take(sizeof(uint32_t));
-  const size_t o_k1 = take(sizeof(K1Partial) * std::max(ws->stream_grid, ws->grid1));
+  const size_t o_k1 = take(sizeof(K1Partial) * ws->stream_grid);
   const size_t o_stats = take(sizeof(StatRec) * STATS_CAP);
   const size_t o_blk = take(sizeof(uint32_t) * 2 * MAX_ROUND_BLOCKS);
   const size_t o_tiles = take(sizeof(unsigned long long) * ws->tiles_cap);
   const size_t o_bits = take(sizeof(uint4) * ((N + 63) / 64));
-  size_t o_lxy[2], o_lis[2], o_tx[2], o_ty[2], o_tid[2], o_sd[3], o_sw[3];
+  size_t o_lxy[2], o_lis[2], o_rc[2], o_tx[2], o_ty[2], o_tid[2], o_sd[3], o_sw[3];
+  // live set runs: K3's CTA j owns [j*run_q, (j+1)*run_q); the rounding of
+  // run_q to whole tiles costs at most one tile per CTA
+  const uint64_t LN = N + 2ull * (uint64_t)di.sm_count * STREAM_T;
   for (int p = 0; p < 2; ++p) {
-    o_lxy[p] = take(16 * N);
-    o_lis[p] = take(8 * N);
+    o_lxy[p] = take(16 * LN);
+    o_lis[p] = take(8 * LN);
+    o_rc[p] = take(4 * MAX_RUNS);
   }
   for (int p = 0; p < 2; ++p) {
     o_tx[p] = take(8 * S);
@@ -169,7 +166,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   }
   for (int p = 0; p < 3; ++p) {
     o_sd[p] = take(8 * S);
-    o_sw[p] = take(4 * S);
+    o_sw[p] = take(sizeof(SlotRec) * S);
   }
   const size_t o_route = take(sizeof(Route) * S);
   CK(cudaMalloc(&ws->arena, off));
@@ -188,13 +185,14 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   for (int p = 0; p < 2; ++p) {
     B.Lxy[p] = (double2*)(a + o_lxy[p]);
     B.Lis[p] = (uint2*)(a + o_lis[p]);
+    B.run_cnt[p] = (uint32_t*)(a + o_rc[p]);
     B.Tx[p] = (double*)(a + o_tx[p]);
     B.Ty[p] = (double*)(a + o_ty[p]);
     B.Tid[p] = (uint32_t*)(a + o_tid[p]);
   }
   for (int p = 0; p < 3; ++p) {
     B.Sd[p] = (unsigned long long*)(a + o_sd[p]);
-    B.Sw[p] = (uint32_t*)(a + o_sw[p]);
+    B.Srec[p] = (SlotRec*)(a + o_sw[p]);
   }
   B.route = (Route*)(a + o_route);
   B.s_cap = (uint32_t)std::min<uint64_t>(s_cap, 0xFFFFFFF0ull);
@@ -205,7 +203,7 @@ void ensure_stage(Workspace& ws, bool ids) {
   if (ws.has_stage && (!ids || ws.has_stage_ids)) return;
   if (ws.stage) CK(cudaFree(ws.stage));
   ws.stage = nullptr;
-  const size_t bytes = 16 * ws.n_cap + (ids ? 4 * ws.n_cap : 0) + 256;
+  const size_t bytes = 2 * align_up(8 * ws.n_cap, 256) + (ids ? align_up(4 * ws.n_cap, 256) : 0);
   CK(cudaMalloc(&ws.stage, bytes));
   ws.has_stage = true;
   ws.has_stage_ids = ids;
@@ -275,15 +273,20 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   const uint64_t n = rq.n;
   const bool host = !(rq.flags & SH_DEVICE_PTRS);
   if (timings) CK(cudaEventRecord(ws.ev[0], st));
-  if (host) {
+  // The TMA bulk copies of K1-K3 need 16-byte aligned x/y/ids: host inputs and
+  // unaligned device inputs go through the workspace's aligned staging copy.
+  const bool aligned = ((uintptr_t)rq.x % 16 == 0) && ((uintptr_t)rq.y % 16 == 0) &&
+                       (!rq.ids || (uintptr_t)rq.ids % 16 == 0);
+  if (host || !aligned) {
     ensure_stage(ws, rq.ids != nullptr);
     B = ws.B;
     double* sx = (double*)ws.stage;
-    double* sy = sx + ws.n_cap;
-    uint32_t* sid = (uint32_t*)(sy + ws.n_cap);
-    CK(cudaMemcpyAsync(sx, rq.x, 8 * n, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(sy, rq.y, 8 * n, cudaMemcpyHostToDevice, st));
-    if (rq.ids) CK(cudaMemcpyAsync(sid, rq.ids, 4 * n, cudaMemcpyHostToDevice, st));
+    double* sy = (double*)((char*)ws.stage + align_up(8 * ws.n_cap, 256));
+    uint32_t* sid = (uint32_t*)((char*)ws.stage + 2 * align_up(8 * ws.n_cap, 256));
+    const cudaMemcpyKind k = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    CK(cudaMemcpyAsync(sx, rq.x, 8 * n, k, st));
+    CK(cudaMemcpyAsync(sy, rq.y, 8 * n, k, st));
+    if (rq.ids) CK(cudaMemcpyAsync(sid, rq.ids, 4 * n, k, st));
     B.in_x = sx;
     B.in_y = sy;
     B.in_id = rq.ids ? sid : nullptr;
@@ -295,29 +298,22 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   if (timings) CK(cudaEventRecord(ws.ev[1], st));
   B.n = (uint32_t)n;
   const bool ids = B.in_id != nullptr;
-  // 16-byte pair loads need 16-byte aligned x/y (8-byte aligned ids)
-  const bool vec = ((uintptr_t)B.in_x % 16 == 0) && ((uintptr_t)B.in_y % 16 == 0) &&
-                   (!ids || (uintptr_t)B.in_id % 8 == 0);
 
-  Ctl init;
-  std::memset(&init, 0, sizeof(init));
-  init.status = ST_RUNNING;
-  init.n = (uint32_t)n;
-  init.mode = (uint32_t)rq.mode;
-  *ws.h_ctl = init;
-  CK(cudaMemcpyAsync(B.ctl, ws.h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  // a zeroed control block is the initial state (ST_RUNNING == 0)
+  CK(cudaMemsetAsync(B.ctl, 0, sizeof(Ctl), st));
 
-  auto grid_for = [&](int full) {
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)full));
-  };
-  launch_k1(B, ids, vec, grid_for(ws.grid1), st);
+  const uint64_t ntiles = (n + STREAM_T - 1) / STREAM_T;
+  const int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ws.stream_grid));
+  B.run_q = (uint32_t)((ntiles + gs - 1) / gs * STREAM_T);
+  launch_k1(B, ids, gs, st);
   if (timings) CK(cudaEventRecord(ws.ev[2], st));
-  launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, ids, vec, grid_for(ws.grid2), st);
+  launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, ids, gs, st);
   if (timings) CK(cudaEventRecord(ws.ev[3], st));
-  launch_k3(B, ids, vec, grid_for(ws.grid3), st);
+  launch_k3(B, ids, gs, st);
   if (timings) CK(cudaEventRecord(ws.ev[4], st));
   CK(cudaGetLastError());
-  CK(launch_rounds(B, ws.rounds_grid, st));
+  // the round kernel's CTA j owns run j of each live set: at most gs runs
+  CK(launch_rounds(B, std::min(ws.rounds_grid, gs), st));
   out.launches = 4;
   if (timings) CK(cudaEventRecord(ws.ev[5], st));
   const bool out_dev = (rq.flags & SH_OUT_DEVICE) != 0;
@@ -479,6 +475,7 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
       res->stats[i].segments = ws->h_stats[i].segments;
       res->stats[i].points_remaining = ws->h_stats[i].points_remaining;
       res->stats[i].points_removed = ws->h_stats[i].points_removed;
+      res->stats[i].end_ns = ws->h_stats[i].end_ns;
     }
     if (timings) {
       auto el = [&](int i, int j) {

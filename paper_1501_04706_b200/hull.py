@@ -132,6 +132,7 @@ class HullResult:
     rounds: int = 0
     kernel_launches: int = 0
     kernels: object = None
+    round_end_ms: list = field(default_factory=list)  # device time at the end of each round
 
     @property
     def vertices(self) -> list:
@@ -222,12 +223,13 @@ def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, st
     nst = min(int(res.rounds), stats_cap)
     sts = [SegmentStats(int(st[i].iteration), int(st[i].segments), int(st[i].points_remaining),
                         int(st[i].points_removed)) for i in range(nst)]
+    ends = [st[i].end_ns * 1e-6 for i in range(nst)]
     ph = PhaseTimings(res.phases.pre_ms, res.phases.split_ms, res.phases.recurse_ms,
                       res.phases.total_ms)
     k = res.kernels
     kt = KernelTimings(k.h2d_ms, k.extremes_ms, k.filter_ms, k.first_round_ms, k.rounds_ms,
                        k.d2h_ms)
-    return res, sts, ph, kt
+    return res, sts, ph, kt, ends
 
 
 def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int | None = None,
@@ -246,13 +248,14 @@ def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int |
     oi = np.empty(capacity, np.int64)
     flags = (_lib.SH_DEVICE_PTRS if dx else _lib.SH_HOST_PTRS) | (
         _lib.SH_PHASE_TIMINGS if timings else 0)
-    res, sts, ph, kt = _call(px, py, n, _ptr_of(ids)[0] if ids is not None else None, mode,
+    res, sts, ph, kt, ends = _call(px, py, n, _ptr_of(ids)[0] if ids is not None else None, mode,
                              flags, device, stream, ox.ctypes.data, oy.ctypes.data,
                              oi.ctypes.data, capacity, (1 << 16) if stats else 0)
     h = int(res.h)
     r = HullResult(ox[:h].copy(), oy[:h].copy(), oi[:h].copy(), sts, ph, int(res.kept),
                    int(res.rounds), int(res.kernel_launches))
     r.kernels = kt
+    r.round_end_ms = ends
     return r
 
 
@@ -269,6 +272,7 @@ class DeviceHull:
     kept: int
     rounds: int
     kernel_launches: int
+    round_end_ms: list = field(default_factory=list)
 
 
 def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int | None = None,
@@ -290,12 +294,12 @@ def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int |
     if stream is None:
         stream = torch.cuda.current_stream(x.device).cuda_stream
     flags = _lib.SH_DEVICE_PTRS | _lib.SH_OUT_DEVICE | (_lib.SH_PHASE_TIMINGS if timings else 0)
-    res, sts, ph, kt = _call(px, py, n, ids.data_ptr() if ids is not None else None, mode, flags,
+    res, sts, ph, kt, ends = _call(px, py, n, ids.data_ptr() if ids is not None else None, mode, flags,
                              device, stream, ox.data_ptr(), oy.data_ptr(), oi.data_ptr(),
                              int(ox.shape[0]), (1 << 16) if stats else 0)
     h = int(res.h)
     return DeviceHull(ox[:h], oy[:h], oi[:h], h, sts, ph, kt, int(res.kept), int(res.rounds),
-                      int(res.kernel_launches))
+                      int(res.kernel_launches), ends)
 
 
 def run(points: PointSet, mode: Mode = Mode.WithPreprocess,

@@ -33,7 +33,7 @@ def test_library_loads_and_exports_header_symbols():
     for s in syms:
         assert hasattr(L, s), f"{s} declared in include/ but not exported"
     assert set(_lib.EXPORTS) == syms
-    assert L.sh_b200_abi_version() == 1
+    assert L.sh_b200_abi_version() == 2
 
 
 def test_library_is_sm100a_cubin():
@@ -80,6 +80,6 @@ def test_host_generators_bit_identical_to_reference_stream():
 
 
 def test_struct_layouts_match_header():
-    assert ctypes.sizeof(_lib.sh_round_stat) == 32
+    assert ctypes.sizeof(_lib.sh_round_stat) == 40
     assert ctypes.sizeof(_lib.sh_phase_ms) == 32
     assert ctypes.sizeof(_lib.sh_hull_request) == 56

@@ -21,3 +21,4 @@ torch.cuda.synchronize()
 for _ in range(reps):
     r = hull.run_device(x, y, 1, timings=True)
     print(kind, n, "h", r.h, "rounds", r.rounds, r.kernels, r.phase_timings, flush=True)
+    print("   round end (ms since K1 start):", [round(t, 4) for t in r.round_end_ms], flush=True)
