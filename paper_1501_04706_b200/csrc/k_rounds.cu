@@ -365,7 +365,8 @@ SH_DEV void rounds_barrier(Ctl* c, uint32_t P) {
 // Route entry of old segment s from head table `pin` and farthest record `cr`.
 SH_DEV Route make_route(const Bufs& B, uint32_t pin, const SlotRec* cr, uint32_t s, uint32_t S,
                         uint32_t Slo, uint32_t ns) {
-  const uint32_t cid = __ldcg(&cr->id);
+  const bool shared = __isShared(cr);
+  const uint32_t cid = shared ? cr->id : __ldcg(&cr->id);
   const bool split = cid != NONE;
   const uint32_t sb = s + 1 == S ? 0u : s + 1;
   Route r;
@@ -373,8 +374,8 @@ SH_DEV Route make_route(const Bufs& B, uint32_t pin, const SlotRec* cr, uint32_t
   r.ay = __ldcg(B.Ty[pin] + s);
   r.bx = __ldcg(B.Tx[pin] + sb);
   r.by = __ldcg(B.Ty[pin] + sb);
-  r.cx = split ? __ldcg(&cr->x) : 0.0;
-  r.cy = split ? __ldcg(&cr->y) : 0.0;
+  r.cx = split ? (shared ? cr->x : __ldcg(&cr->x)) : 0.0;
+  r.cy = split ? (shared ? cr->y : __ldcg(&cr->y)) : 0.0;
   r.cid = cid;
   r.ns = ns;
   r.flags = (split ? RT_SPLIT : 0u) | (s < Slo ? RT_LOWER : 0u);
@@ -394,20 +395,24 @@ SH_DEV void write_heads(const Bufs& B, uint32_t pin, uint32_t pout, const Route&
 }
 
 // Small table (S <= SMALL_S), rebuilt by every participating CTA in smem.
-// CTA 0 also writes the next head table.  Returns S', S'lo.
+// CTA 0 also writes the next head table.  The farthest records of the
+// current segments come from the global slots, or -- when the previous round
+// ran on this single CTA -- straight from its shared-memory slots.
+// Returns S', S'lo.
 SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, uint32_t pin,
-                        uint32_t pout, uint32_t sin, uint32_t* s_ws, uint32_t& Sn,
-                        uint32_t& Slon) {
+                        uint32_t pout, uint32_t sin, bool from_smem, uint32_t* s_ws,
+                        uint32_t& Sn, uint32_t& Slon) {
   const bool heads = blockIdx.x == 0;
+  const SlotRec* recs = from_smem ? sm.rec : B.Srec[sin];
   uint32_t running = 0, lower_splits = 0;
   for (uint32_t s0 = 0; s0 < S; s0 += RTPB) {
     const uint32_t s = s0 + threadIdx.x;
-    const uint32_t split = (s < S && __ldcg(&B.Srec[sin][s].id) != NONE) ? 1u : 0u;
+    const uint32_t split = (s < S && (from_smem ? recs[s].id : __ldcg(&recs[s].id)) != NONE) ? 1u : 0u;
     uint32_t total;
     const uint32_t pre = block_exclusive_scan(split, s_ws, &total);
     lower_splits += (uint32_t)__syncthreads_count(split && s < Slo);
     if (s < S) {
-      const Route r = make_route(B, pin, B.Srec[sin] + s, s, S, Slo, s + running + pre);
+      const Route r = make_route(B, pin, recs + s, s, S, Slo, s + running + pre);
       sm.rt[s] = r;
       if (heads) write_heads(B, pin, pout, r, s);
     }
@@ -415,6 +420,7 @@ SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, 
   }
   Sn = S + running;
   Slon = Slo + lower_splits;
+  __syncthreads();  // every route is built before the records are recycled
   for (uint32_t t = threadIdx.x; t < Sn; t += RTPB) rec_clear(&sm.db[t], &sm.rec[t]);
   __syncthreads();
 }
@@ -479,6 +485,8 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   return true;
 }
 
+constexpr uint32_t ROUND_TARGET = 8192;  // live points per active CTA before CTAs retire
+
 __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RoundSmem& sm = *reinterpret_cast<RoundSmem*>(smem_raw);
@@ -493,27 +501,46 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   uint32_t m = *(volatile uint32_t*)&c->m_cur;
   uint32_t nruns = *(volatile uint32_t*)&c->nruns;
   const uint32_t n = B.n, q = B.run_q;
+  const uint32_t target = min(ROUND_TARGET, q);
   uint32_t P = gridDim.x;
+  bool recs_smem = false;  // this round's input records live in this CTA's smem
 
   while (true) {
-    if (P > 1 && m <= TAIL_M) {  // every CTA sees the same m: consistent
-      P = 1;
-      if (blockIdx.x != 0) return;
+    // active CTAs for this round: ~ROUND_TARGET live points each (m only
+    // shrinks, so retired CTAs never need to come back); every CTA sees the
+    // same m, so the decision is consistent
+    {
+      const uint32_t want = max(1u, min(P, (m + target - 1) / target));
+      if (blockIdx.x >= want) return;
+      P = want;
     }
     const uint32_t pin = (r - 1) & 1u, pout = r & 1u;
     const uint32_t sin = (r - 1) % 3u, sout = r % 3u, sres = (r + 1) % 3u;
     const bool small = S <= (uint32_t)SMALL_S;
     uint32_t Sn, Slon;
     if (small) {
-      table_small(B, sm, S, Slo, pin, pout, sin, s_ws, Sn, Slon);
+      table_small(B, sm, S, Slo, pin, pout, sin, recs_smem, s_ws, Sn, Slon);
     } else if (!table_large(B, S, Slo, pin, pout, sin, P, s_ws, Sn, Slon)) {
       return;
     }
-    // clear round r+1's farthest slots (at most 2 Sn segments)
+    // clear round r+1's global farthest slots (at most 2 Sn segments)
     {
       const uint32_t lim = min(2 * Sn, B.s_cap);
       for (uint32_t t = blockIdx.x * RTPB + threadIdx.x; t < lim; t += P * RTPB)
         rec_clear(B.Sd[sres] + t, B.Srec[sres] + t);
+    }
+    // prefix of the input run counts: the live set as one virtual range
+    {
+      uint32_t tot;
+      for (uint32_t j0 = 0; j0 < nruns; j0 += RTPB) {
+        const uint32_t j = j0 + threadIdx.x;
+        const uint32_t v = j < nruns ? (nruns == 1 ? m : __ldcg(B.run_cnt[pin] + j)) : 0u;
+        const uint32_t base0 = j0 ? s_pref[j0] : 0u;
+        const uint32_t ex = block_exclusive_scan(v, s_ws, &tot);
+        if (j < nruns) s_pref[j] = base0 + ex;
+        if (threadIdx.x == 0) s_pref[min(j0 + RTPB, nruns)] = base0 + tot;
+        __syncthreads();
+      }
     }
     if (threadIdx.x == 0) {
       s_off = 0;
@@ -521,19 +548,30 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     }
     __syncthreads();
 
-    // ---- point phase: this CTA's runs of the live set -> its run of the next ----
+    // ---- point phase: virtual range [lo, hi) of the live set -> run j ----
     const double2* Ixy = B.Lxy[pin];
     const uint2* Iis = B.Lis[pin];
     double2* Oxy = B.Lxy[pout];
     uint2* Ois = B.Lis[pout];
     unsigned long long* Sd = B.Sd[sout];
     SlotRec* Srec = B.Srec[sout];
-    const uint32_t obase = (P == 1 ? 0u : blockIdx.x) * q;
+    const uint32_t obase = blockIdx.x * q;
+    const uint32_t lo = (uint32_t)((unsigned long long)m * blockIdx.x / P);
+    const uint32_t hi = (uint32_t)((unsigned long long)m * (blockIdx.x + 1) / P);
     uint32_t k = 0;
-    // One tile of live points: element e < cnt of the range `map` resolves.
-    auto do_tile = [&](uint32_t t0, uint32_t cnt, auto map) {
+    for (uint32_t t0 = lo; t0 < hi; t0 += KR_TILE) {
       if (small && k) resolve_list(sm.db, sm.rec, sm.cl, (k - 1) % 3u);
       if (small && threadIdx.x == 0) sm.cl.n[(k + 1) % 3u] = 0;
+      // run containing the tile start (binary search; points walk forward)
+      uint32_t rb = 0;
+      {
+        uint32_t a0 = 0, a1 = nruns;
+        while (a1 - a0 > 1) {
+          const uint32_t mid = (a0 + a1) >> 1;
+          if (s_pref[mid] <= t0) a0 = mid; else a1 = mid;
+        }
+        rb = a0;
+      }
       double px[KR_U], py[KR_U], pd[KR_U];
       uint32_t pid[KR_U], pseg[KR_U], oseg[KR_U];
       uint32_t keepm = 0, lowm = 0;
@@ -543,8 +581,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
         px[u] = py[u] = 0.0;
         pid[u] = 0;
         oseg[u] = NONE;
-        if (e < cnt) {
-          const uint32_t ph = map(e);
+        if (e < hi) {
+          uint32_t b2 = rb;
+          while (e >= s_pref[b2 + 1]) ++b2;
+          const uint32_t ph = b2 * q + (e - s_pref[b2]);
           const double2 v = __ldcg(Ixy + ph);
           const uint2 is = __ldcg(Iis + ph);
           px[u] = v.x;
@@ -578,52 +618,19 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase);
       __syncthreads();
       ++k;
-    };
-    if (P == 1 && nruns > 1) {
-      // single CTA over many runs: walk them as one virtual range through an
-      // smem prefix of the run counts (binary search per point)
-      uint32_t* pref = s_pref;
-      uint32_t tot;
-      for (uint32_t j0 = 0; j0 < nruns; j0 += RTPB) {
-        const uint32_t j = j0 + threadIdx.x;
-        const uint32_t v = j < nruns ? __ldcg(B.run_cnt[pin] + j) : 0u;
-        const uint32_t base0 = j0 ? pref[j0] : 0u;
-        const uint32_t ex = block_exclusive_scan(v, s_ws, &tot);
-        if (j < nruns) pref[j] = base0 + ex;
-        if (j0 + RTPB >= nruns && threadIdx.x == 0) pref[nruns] = base0 + tot;
-        __syncthreads();
-        if (j0 + RTPB < nruns && threadIdx.x == 0) pref[j0 + RTPB] = base0 + tot;
-        __syncthreads();
-      }
-      const uint32_t total = pref[nruns];
-      auto map = [&](uint32_t e) {
-        uint32_t lo = 0, hi = nruns;  // pref[lo] <= e < pref[hi]
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (pref[mid] <= e) lo = mid; else hi = mid;
-        }
-        return lo * q + (e - pref[lo]);
-      };
-      for (uint32_t t0 = 0; t0 < total; t0 += KR_TILE) do_tile(t0, total, map);
-    } else {
-      for (uint32_t run = blockIdx.x; run < nruns; run += P) {
-        const uint32_t rc = __ldcg(B.run_cnt[pin] + run);
-        const uint32_t ibase = run * q;
-        auto map = [ibase](uint32_t e) { return ibase + e; };
-        for (uint32_t t0 = 0; t0 < rc; t0 += KR_TILE) do_tile(t0, rc, map);
-      }
     }
+    // a lone CTA whose next table is small keeps its records in smem
+    const bool keep_smem = small && P == 1 && Sn <= (uint32_t)SMALL_S;
     if (small) {
       if (k) resolve_list(sm.db, sm.rec, sm.cl, (k - 1) % 3u);
       __syncthreads();
-      flush_slots(sm.db, sm.rec, Sn, Slon, Sd, Srec);
+      if (!keep_smem) flush_slots(sm.db, sm.rec, Sn, Slon, Sd, Srec);
     }
-    const uint32_t nruns_out = P == 1 ? 1u : P;
-    if (threadIdx.x == 0) B.run_cnt[pout][P == 1 ? 0u : blockIdx.x] = s_off;
+    if (threadIdx.x == 0) B.run_cnt[pout][blockIdx.x] = s_off;
     rounds_barrier(c, P);
 
     // ---- close round r (every participating CTA computes the same) ----
-    const uint32_t mn = sum_runs(B.run_cnt[pout], nruns_out, s_ws);
+    const uint32_t mn = P == 1 ? *(volatile uint32_t*)&s_off : sum_runs(B.run_cnt[pout], P, s_ws);
     if (blockIdx.x == 0 && threadIdx.x == 0 && r <= (uint32_t)STATS_CAP) {
       StatRec st;
       st.segments = Sn;
@@ -636,7 +643,8 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     S = Sn;
     Slo = Slon;
     m = mn;
-    nruns = nruns_out;
+    nruns = P;
+    recs_smem = keep_smem;
     if (mn == 0 || r + 1 > n) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         c->round = r;
