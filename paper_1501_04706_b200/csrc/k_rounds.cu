@@ -425,20 +425,31 @@ SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, 
   __syncthreads();
 }
 
-// Large table: a grid-wide two-step scan over the P participating CTAs.
+// Large table: a grid-wide two-step scan over the P participating CTAs, each
+// thread owning TS consecutive segments (independent loads in flight).  The
+// table also clears the global farthest slots of the segments it creates.
 // Returns false on segment-table overflow (every CTA returns consistently).
+constexpr int TS = 8;
+
 SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, uint32_t pout,
-                        uint32_t sin, uint32_t P, uint32_t* s_ws, uint32_t& Sn,
+                        uint32_t sin, uint32_t sout, uint32_t P, uint32_t* s_ws, uint32_t& Sn,
                         uint32_t& Slon) {
   Ctl* c = B.ctl;
   const uint32_t per = (S + P - 1) / P;
   const uint32_t lo = min(S, blockIdx.x * per), hi = min(S, lo + per);
+  const SlotRec* recs = B.Srec[sin];
   // T1: splittable counts of this CTA's range (total and lower chain)
   uint32_t cnt = 0, cnt_lo = 0;
-  for (uint32_t s = lo + threadIdx.x; s < hi; s += RTPB) {
-    const bool split = __ldcg(&B.Srec[sin][s].id) != NONE;
-    cnt += split;
-    cnt_lo += split && s < Slo;
+  for (uint32_t s0 = lo + threadIdx.x * TS; s0 < hi; s0 += RTPB * TS) {
+    uint32_t ids[TS];
+#pragma unroll
+    for (int i = 0; i < TS; ++i) ids[i] = s0 + i < hi ? __ldcg(&recs[s0 + i].id) : NONE;
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      const bool split = ids[i] != NONE;
+      cnt += split;
+      cnt_lo += split && s0 + i < Slo;
+    }
   }
   {
     uint32_t t1, t2;
@@ -469,15 +480,28 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
     return false;
   }
   uint32_t running = pre_all;
-  for (uint32_t s0 = lo; s0 < hi; s0 += RTPB) {
-    const uint32_t s = s0 + threadIdx.x;
-    const uint32_t split = (s < hi && __ldcg(&B.Srec[sin][s].id) != NONE) ? 1u : 0u;
+  for (uint32_t g0 = lo; g0 < hi; g0 += RTPB * TS) {
+    const uint32_t s0 = g0 + threadIdx.x * TS;
+    uint32_t ids[TS];
+    uint32_t mine = 0;
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      ids[i] = s0 + i < hi ? __ldcg(&recs[s0 + i].id) : NONE;
+      mine += ids[i] != NONE;
+    }
     uint32_t total;
-    const uint32_t p = block_exclusive_scan(split, s_ws, &total);
-    if (s < hi) {
-      const Route r = make_route(B, pin, B.Srec[sin] + s, s, S, Slo, s + running + p);
-      B.route[s] = r;
-      write_heads(B, pin, pout, r, s);
+    uint32_t ns = s0 + running + block_exclusive_scan(mine, s_ws, &total);
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      const uint32_t s = s0 + i;
+      if (s < hi) {
+        const Route r = make_route(B, pin, recs + s, s, S, Slo, ns);
+        B.route[s] = r;
+        write_heads(B, pin, pout, r, s);
+        rec_clear(B.Sd[sout] + ns, B.Srec[sout] + ns);
+        if (r.flags & RT_SPLIT) rec_clear(B.Sd[sout] + ns + 1, B.Srec[sout] + ns + 1);
+        ns += (r.flags & RT_SPLIT) ? 2u : 1u;
+      }
     }
     running += total;
   }
@@ -510,7 +534,8 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     // shrinks, so retired CTAs never need to come back); every CTA sees the
     // same m, so the decision is consistent
     {
-      const uint32_t want = max(1u, min(P, (m + target - 1) / target));
+      const uint32_t work = max(m, S);  // live points, or segments of a large table
+      const uint32_t want = max(1u, min(P, (work + target - 1) / target));
       if (blockIdx.x >= want) return;
       P = want;
     }
@@ -520,11 +545,12 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     uint32_t Sn, Slon;
     if (small) {
       table_small(B, sm, S, Slo, pin, pout, sin, recs_smem, s_ws, Sn, Slon);
-    } else if (!table_large(B, S, Slo, pin, pout, sin, P, s_ws, Sn, Slon)) {
+    } else if (!table_large(B, S, Slo, pin, pout, sin, sout, P, s_ws, Sn, Slon)) {
       return;
     }
-    // clear round r+1's global farthest slots (at most 2 Sn segments)
-    {
+    // clear round r+1's global farthest slots (at most 2 Sn segments) when
+    // round r+1 will use a small table; a large table clears its own slots
+    if (Sn <= (uint32_t)SMALL_S) {
       const uint32_t lim = min(2 * Sn, B.s_cap);
       for (uint32_t t = blockIdx.x * RTPB + threadIdx.x; t < lim; t += P * RTPB)
         rec_clear(B.Sd[sres] + t, B.Srec[sres] + t);
@@ -606,14 +632,12 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       if (small) {
         contend_tile<KR_U>(sm.db, sm.rec, sm.cl, k, keepm, px, py, pd, pid, pseg, lowm);
       } else {
+        // large table: fire-and-forget max of the distance bits; the winners
+        // are identified after the barrier (winner pass below)
 #pragma unroll
-        for (int u = 0; u < KR_U; ++u) {
-          if ((keepm >> u) & 1u) {
-            Cand me;
-            me.d = pd[u]; me.x = px[u]; me.y = py[u]; me.id = pid[u]; me.pos = 0;
-            rec_offer(Sd + pseg[u], Srec + pseg[u], me, (lowm >> u) & 1u);
-          }
-        }
+        for (int u = 0; u < KR_U; ++u)
+          if ((keepm >> u) & 1u)
+            atomicMax(Sd + pseg[u], (unsigned long long)__double_as_longlong(pd[u]));
       }
       run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase);
       __syncthreads();
@@ -628,6 +652,28 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     }
     if (threadIdx.x == 0) B.run_cnt[pout][blockIdx.x] = s_off;
     rounds_barrier(c, P);
+    if (!small) {
+      // winner pass: every survivor of this CTA (its run, still hot in L2)
+      // recomputes its distance against its new segment's base line -- the
+      // same RN operations as in routing, so bit-identical -- and the ones at
+      // the slot maximum settle the comparator's ties under the record lock
+      const double* Hx = B.Tx[pout];
+      const double* Hy = B.Ty[pout];
+      const uint32_t cnt = *(volatile uint32_t*)&s_off;
+      for (uint32_t e = threadIdx.x; e < cnt; e += RTPB) {
+        const double2 v = __ldcg(Oxy + obase + e);
+        const uint2 is = __ldcg(Ois + obase + e);
+        const uint32_t t = is.y, t1 = t + 1 == Sn ? 0u : t + 1;
+        const double d = outward_e(make_edge(__ldcg(Hx + t), __ldcg(Hy + t), __ldcg(Hx + t1),
+                                             __ldcg(Hy + t1)), v.x, v.y);
+        if ((unsigned long long)__double_as_longlong(d) == __ldcg(Sd + t)) {
+          Cand me;
+          me.d = d; me.x = v.x; me.y = v.y; me.id = is.x; me.pos = 0;
+          rec_update<false>(Srec + t, me, t < Slon);
+        }
+      }
+      rounds_barrier(c, P);
+    }
 
     // ---- close round r (every participating CTA computes the same) ----
     const uint32_t mn = P == 1 ? *(volatile uint32_t*)&s_off : sum_runs(B.run_cnt[pout], P, s_ws);
