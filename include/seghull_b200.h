@@ -68,7 +68,9 @@ typedef struct {
   uint64_t segments;
   uint64_t points_remaining;
   uint64_t points_removed;
-  uint64_t end_ns;  /* %globaltimer at the end of the round, relative to the start of K1 */
+  uint64_t end_ns;     /* %globaltimer at the end of the round, relative to the start of K1 */
+  uint64_t table_ns;   /* ... when the segment-table phase ended (CTA 0; 0 for round 1)   */
+  uint64_t points_ns;  /* ... when the point phase ended (CTA 0; 0 for round 1)           */
 } sh_round_stat;
 
 /* hull.hpp:42-46 PhaseTimings (device time from CUDA events) */

@@ -20,7 +20,8 @@ _vp = ctypes.c_void_p
 
 class sh_round_stat(ctypes.Structure):
     _fields_ = [("iteration", _u64), ("segments", _u64),
-                ("points_remaining", _u64), ("points_removed", _u64), ("end_ns", _u64)]
+                ("points_remaining", _u64), ("points_removed", _u64), ("end_ns", _u64),
+                ("table_ns", _u64), ("points_ns", _u64)]
 
 
 class sh_phase_ms(ctypes.Structure):

@@ -366,6 +366,10 @@ SH_DEV void tma_load_1d(void* dst, const void* src, uint32_t bytes, unsigned lon
       : "memory");
 }
 
+SH_DEV void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 SH_DEV void mbar_wait(unsigned long long* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -387,12 +391,13 @@ struct TileRing {
   // AUX: bytes per 64-point chunk of an optional side stream (K3: the chain bits)
   static constexpr size_t kAuxBytes = (size_t)(T / 64) * AUX;
   static constexpr size_t kStageBytes = (size_t)T * (16 + (IDS ? 4 : 0)) + kAuxBytes;
-  static constexpr size_t kBytes = NS * kStageBytes + NS * sizeof(unsigned long long);
+  static constexpr size_t kBytes = NS * kStageBytes + 2 * NS * sizeof(unsigned long long);
   double* xs;                 // [NS][T]
   double* ys;                 // [NS][T]
   uint32_t* is;               // [NS][T] when IDS
   unsigned char* aux;         // [NS][kAuxBytes]
-  unsigned long long* bar;    // [NS]
+  unsigned long long* bar;    // [NS] full: the stage's bytes landed
+  unsigned long long* ebar;   // [NS] empty: every consumer warp is done with it
 
   SH_DEV void carve(unsigned char* base) {
     xs = reinterpret_cast<double*>(base);
@@ -400,9 +405,13 @@ struct TileRing {
     is = reinterpret_cast<uint32_t*>(ys + NS * T);
     aux = reinterpret_cast<unsigned char*>(is + (IDS ? NS * T : 0));
     bar = reinterpret_cast<unsigned long long*>(base + NS * kStageBytes);
+    ebar = bar + NS;
   }
   SH_DEV void init() {  // thread 0, followed by __syncthreads by the caller
-    for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(bar + s, 1);
+      mbar_init(ebar + s, CWARPS);
+    }
     mbar_fence_init();
   }
   // thread 0: stream points [first, first + cnt) into stage s
@@ -425,6 +434,11 @@ struct TileRing {
     if (ab) tma_load_1d(aux + s * kAuxBytes, A + (size_t)(first / 64) * AUX, ab, bar + s);
   }
   SH_DEV void wait(int s, uint32_t parity) { mbar_wait(bar + s, parity); }
+  // one arrival per warp when the warp no longer reads stage s
+  SH_DEV void release(int s) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(ebar + s);
+  }
 };
 
 }  // namespace shb
@@ -432,9 +446,12 @@ struct TileRing {
 namespace shb {
 
 // Streams this CTA's share of the input through the ring: tiles b, b+G, ...
-// (mapped to ntiles-1-t when `reverse`), calling body(stage, first, cnt) for
-// each after its bytes landed.  A __syncthreads follows each body before the
-// stage is refilled.  The caller initialised the ring (+ __syncthreads).
+// (mapped to ntiles-1-t when `reverse`), calling body(stage, first, cnt) in
+// the CWARPS consumer warps for each tile after its bytes landed.  Warp
+// CWARPS is a dedicated producer: it refills a stage as soon as every
+// consumer warp released it (empty mbarrier), so no consumer ever waits for
+// another consumer and no CTA-wide barrier is needed per tile.  The caller
+// initialised the ring (+ __syncthreads); a __syncthreads ends the stream.
 template <int T, int NS, bool IDS, int AUX, class Body>
 SH_DEV void stream_input(TileRing<T, NS, IDS, AUX>& R, uint32_t n, const double* X,
                          const double* Y, const uint32_t* I, const unsigned char* A, bool reverse,
@@ -446,23 +463,25 @@ SH_DEV void stream_input(TileRing<T, NS, IDS, AUX>& R, uint32_t n, const double*
     const uint32_t t = b + k * G;
     return reverse ? ntiles - 1 - t : t;
   };
-  if (threadIdx.x == 0) {
-    for (uint32_t k = 0; k < mine && k < (uint32_t)NS; ++k) {
+  if ((int)(threadIdx.x >> 5) == CWARPS) {  // producer warp
+    if ((threadIdx.x & 31) == 0) {
+      for (uint32_t k = 0; k < mine; ++k) {
+        const int s = (int)(k % NS);
+        if (k >= (uint32_t)NS) mbar_wait(R.ebar + s, ((k / NS) - 1) & 1u);
+        const uint32_t first = tile_of(k) * T;
+        R.issue(s, X, Y, I, first, min((uint32_t)T, n - first), A);
+      }
+    }
+  } else {
+    for (uint32_t k = 0; k < mine; ++k) {
+      const int s = (int)(k % NS);
+      R.wait(s, (k / NS) & 1u);
       const uint32_t first = tile_of(k) * T;
-      R.issue((int)k, X, Y, I, first, min((uint32_t)T, n - first), A);
+      body(s, first, min((uint32_t)T, n - first));
+      R.release(s);
     }
   }
-  for (uint32_t k = 0; k < mine; ++k) {
-    const int s = (int)(k % NS);
-    R.wait(s, (k / NS) & 1u);
-    const uint32_t first = tile_of(k) * T;
-    body(s, first, min((uint32_t)T, n - first));
-    __syncthreads();
-    if (threadIdx.x == 0 && k + NS < mine) {
-      const uint32_t f2 = tile_of(k + NS) * T;
-      R.issue(s, X, Y, I, f2, min((uint32_t)T, n - f2), A);
-    }
-  }
+  __syncthreads();
 }
 
 }  // namespace shb

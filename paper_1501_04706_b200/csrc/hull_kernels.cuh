@@ -10,7 +10,9 @@
 //   live set     ping-pong {xy double2, (id, seg) uint2}[cap]    24 B/point,
 //                organised as RUNS: run j occupies [j*run_q, j*run_q + cnt_j);
 //                CTA j of a round writes its survivors densely into run j
-//                (CTA-local offsets, no global atomics), run_cnt[par][j] = cnt_j
+//                (CTA-local offsets, no global atomics), run_cnt[par][j] = cnt_j;
+//                an odd run is padded with one dead entry (seg = NONE) so
+//                every run can be fetched with 16-byte bulk copies
 //   head table   ping-pong {x f64, y f64, id u32}[S]              20 B/segment
 //   farthest     3-way rotating slots {dbits u64, SlotRec 32 B}[S] 40 B/segment
 //   route table  Route[S] 64 B (large tables only; small ones live in smem)
@@ -36,22 +38,26 @@ constexpr int WARPS = TPB / 32;
 constexpr int RTPB = 512;            // persistent round kernel
 constexpr int STPB = 512;            // TMA-fed streaming kernels K1/K2/K3 (one CTA per SM)
 constexpr int SWARPS = STPB / 32;
+constexpr int CWARPS = SWARPS - 1;   // consumer warps; warp CWARPS is the TMA producer
+constexpr int CTHREADS = 32 * CWARPS;
 #ifndef SHB_STREAM_T
-#define SHB_STREAM_T 2048
+#define SHB_STREAM_T 1920
 #endif
 #ifndef SHB_STREAM_NS
 #define SHB_STREAM_NS 4
 #endif
 constexpr int STREAM_T = SHB_STREAM_T;    // points per TMA tile
 constexpr int STREAM_NS = SHB_STREAM_NS;  // ring stages (NS-1 tiles in flight while one is consumed)
-constexpr int SMALL_S = 1024;        // tables up to this size are rebuilt per CTA in smem
+constexpr int SMALL_S = 512;         // tables up to this size are rebuilt per CTA in smem
 constexpr int NSLOT = 2 * SMALL_S;   // next-round segments of a small table
 constexpr uint32_t TAIL_M = 4096;    // live sets up to this size finish in one CTA
 constexpr int STATS_CAP = 1 << 16;
 constexpr int STATS_EAGER = 64;      // stats read back together with the control block
 constexpr int MAX_ROUND_BLOCKS = 1024;
 constexpr int MAX_RUNS = MAX_ROUND_BLOCKS;
-constexpr int CLIST = 256;           // phase-B contender list entries per tile
+constexpr int CLIST = 128;           // phase-B contender list entries per tile
+constexpr int LIVE_T = 2 * CTHREADS;  // live points per TMA tile of the round kernel (960)
+constexpr int LIVE_NS = 6;           // its ring stages
 
 enum Status : uint32_t {
   ST_RUNNING = 0,
@@ -97,7 +103,9 @@ struct __align__(16) SlotRec {
 
 struct StatRec {
   uint32_t segments, points_remaining, points_removed, pad;
-  unsigned long long end_ns;  // %globaltimer at the end of the round (minus Ctl::t0_ns)
+  unsigned long long end_ns;     // %globaltimer at the end of the round (minus Ctl::t0_ns)
+  unsigned long long table_ns;   // ... when CTA 0 finished the segment-table phase
+  unsigned long long points_ns;  // ... when CTA 0 finished its point phase
 };
 
 // Device-resident control block.  The host writes it once per call and
@@ -125,6 +133,9 @@ struct Ctl {
   uint32_t tile_ctr;    // generator scratch
   uint32_t m_next;      // generator scratch
   unsigned long long t0_ns;  // %globaltimer when K1 started (per-round timestamps)
+  unsigned long long tl[32]; // debug timeline of CTA 0 (sh_b200_last_timeline)
+  uint32_t tl_round;         // round whose tiles are traced (0: none)
+  uint32_t tl_n;
 };
 
 struct Bufs {
@@ -141,6 +152,7 @@ struct Bufs {
   StatRec* stats;
   unsigned long long* tile_status;
   uint32_t* blk_cnt;      // [2 * MAX_ROUND_BLOCKS] per-CTA counts of a large table scan
+  unsigned long long* dbg;  // [MAX_ROUND_BLOCKS] debug: per-CTA point-phase end of the traced round
   // classification bits
   uint4* bits;
   // live set (runs)

@@ -186,8 +186,8 @@ __global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
     bool moved = false;
     if (cnt == (uint32_t)STREAM_T) {
 #pragma unroll
-      for (int k = 0; k < STREAM_T / 2 / STPB; ++k) {
-        const uint32_t p = k * STPB + threadIdx.x;
+      for (int k = 0; k < STREAM_T / 2 / CTHREADS; ++k) {
+        const uint32_t p = k * CTHREADS + threadIdx.x;
         const double2 xv = reinterpret_cast<const double2*>(xs)[p];
         const double2 yv = reinterpret_cast<const double2*>(ys)[p];
         // can either point reach an extreme, or is it non-finite (exponent
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
       }
     } else {
       const uint32_t c4 = cnt & ~3u;
-      for (uint32_t j = threadIdx.x; j < cnt; j += STPB) {
+      for (uint32_t j = threadIdx.x; j < cnt; j += CTHREADS) {
         const uint32_t i = first + j;
         const bool sm = j < c4;
         const double x = sm ? xs[j] : __ldg(X + i);
@@ -364,57 +364,29 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
     return __dsub_rn(__dmul_rn(ex, dy), __dmul_rn(ey, dx));
   };
 
-  // one point: returns (keep, lower member, upper member) bits
-  auto visit = [&](double x, double y, uint32_t i, uint32_t id, bool valid) -> uint32_t {
-    const double dxL = __dsub_rn(x, cxL), dyL = __dsub_rn(y, cyL);
-    const double dxR = __dsub_rn(x, cxR), dyR = __dsub_rn(y, cyR);
-    const double cl = xprod(E01.ex, E01.ey, dxL, dyL);  // cross(P0, Pr, p)
-    bool inside = false;
-    if (quad4) {  // hull.cpp:80-90: discard iff cross > 0 for every edge
-      const double dxB = __dsub_rn(x, cxB), dyB = __dsub_rn(y, cyB);
-      const double dxT = __dsub_rn(x, cxT), dyT = __dsub_rn(y, cyT);
-      inside = valid & (xprod(Q[0].ex, Q[0].ey, dxL, dyL) > 0.0) &
-               (xprod(Q[1].ex, Q[1].ey, dxB, dyB) > 0.0) &
-               (xprod(Q[2].ex, Q[2].ey, dxR, dyR) > 0.0) &
-               (xprod(Q[3].ex, Q[3].ey, dxT, dyT) > 0.0);
-    } else if (filt) {  // degenerate quadrilateral (3 distinct corners)
-      inside = valid;
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq)
-        if (qq < ne) inside = inside && (cross_e(Q[qq], x, y) > 0.0);
-    }
-    const bool keep = valid && !inside;
-    noncol = noncol || (valid && cl != 0.0);
-    const bool member = keep && i != p0 && i != pr;
-    const bool lw = member && cl < 0.0;  // hull.cpp:115-117
-    const bool up = member && !(cl < 0.0);
-    if (lw) {
-      cand_visit(a0, -cl, x, y, id, i, true);  // outward_distance(P0, Pr, p)
-    } else if (up) {
-      cand_visit(a1, -xprod(E10.ex, E10.ey, dxR, dyR), x, y, id, i, false);  // outward_distance(Pr, P0, p)
-    }
-    return (uint32_t)keep | ((uint32_t)lw << 1) | ((uint32_t)up << 2);
-  };
-
   // backwards over the input: K1 just left the tail in L2, K3 starts at the head
+  constexpr int NCH = STREAM_T / 64 / CWARPS;  // chunks per consumer warp per tile
+  constexpr int NP = 2 * NCH;                  // points per thread per tile
   stream_input(R, n, X, Y, I, nullptr, true, [&](int s, uint32_t first, uint32_t cnt) {
     const double* xs = R.xs + s * STREAM_T;
     const double* ys = R.ys + s * STREAM_T;
     const uint32_t* is = R.is + s * STREAM_T;
     const uint32_t c4 = cnt & ~3u;
+    double px[NP], py[NP];
+    uint32_t pid[NP];
+    bool pv[NP];
+    // ---- gather the thread's points (pairs of one 64-point chunk) ----
 #pragma unroll
-    for (int k = 0; k < STREAM_T / 64 / SWARPS; ++k) {
-      const uint32_t cc = k * SWARPS + warp;  // chunk of 64 points within the tile
-      if (cc * 64 >= cnt) break;              // warp-uniform
-      const uint32_t j = cc * 64 + 2 * lane;  // this lane's pair
-      double2 xv, yv;
+    for (int kk = 0; kk < NCH; ++kk) {
+      const uint32_t cc = kk * CWARPS + warp;  // chunk of 64 points within the tile
+      const uint32_t j = cc * 64 + 2 * lane;   // this lane's pair
+      double2 xv = make_double2(0.0, 0.0), yv = xv;
       uint2 iv = make_uint2(0u, 0u);
       if (j + 1 < c4) {
         xv = reinterpret_cast<const double2*>(xs)[j >> 1];
         yv = reinterpret_cast<const double2*>(ys)[j >> 1];
         if (IDS) iv = reinterpret_cast<const uint2*>(is)[j >> 1];
       } else {
-        xv = yv = make_double2(0.0, 0.0);
         for (int h = 0; h < 2; ++h) {
           const uint32_t jj = j + h;
           if (jj < cnt) {
@@ -425,12 +397,66 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
           }
         }
       }
-      const uint32_t i = first + j;
-      const uint32_t f0 = visit(xv.x, yv.x, i, IDS ? iv.x : i, j < cnt);
-      const uint32_t f1 = visit(xv.y, yv.y, i + 1, IDS ? iv.y : i + 1, j + 1 < cnt);
-      const uint32_t le = __ballot_sync(FULL, f0 & 2u), lodd = __ballot_sync(FULL, f1 & 2u);
-      const uint32_t ue = __ballot_sync(FULL, f0 & 4u), uodd = __ballot_sync(FULL, f1 & 4u);
-      kept += (f0 & 1u) + (f1 & 1u);
+      px[2 * kk] = xv.x; px[2 * kk + 1] = xv.y;
+      py[2 * kk] = yv.x; py[2 * kk + 1] = yv.y;
+      pid[2 * kk] = IDS ? iv.x : first + j;
+      pid[2 * kk + 1] = IDS ? iv.y : first + j + 1;
+      pv[2 * kk] = j < cnt;
+      pv[2 * kk + 1] = j + 1 < cnt;
+    }
+    // ---- arithmetic of all NP points in one branch-free block ----
+    // (the RN operations of cross(), geometry.hpp:17-19, with the per-point
+    // differences to the 4 corners shared by the 6 cross products)
+    double cl[NP], du[NP];
+    bool ins[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const double x = px[q], y = py[q];
+      const double dxL = __dsub_rn(x, cxL), dyL = __dsub_rn(y, cyL);
+      const double dxR = __dsub_rn(x, cxR), dyR = __dsub_rn(y, cyR);
+      cl[q] = xprod(E01.ex, E01.ey, dxL, dyL);         // cross(P0, Pr, p)
+      du[q] = -xprod(E10.ex, E10.ey, dxR, dyR);        // outward_distance(Pr, P0, p)
+      bool inside = false;
+      if (quad4) {  // hull.cpp:80-90: discard iff cross > 0 for every edge
+        const double dxB = __dsub_rn(x, cxB), dyB = __dsub_rn(y, cyB);
+        const double dxT = __dsub_rn(x, cxT), dyT = __dsub_rn(y, cyT);
+        inside = (xprod(Q[0].ex, Q[0].ey, dxL, dyL) > 0.0) &
+                 (xprod(Q[1].ex, Q[1].ey, dxB, dyB) > 0.0) &
+                 (xprod(Q[2].ex, Q[2].ey, dxR, dyR) > 0.0) &
+                 (xprod(Q[3].ex, Q[3].ey, dxT, dyT) > 0.0);
+      } else if (filt) {  // degenerate quadrilateral (3 distinct corners)
+        inside = true;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+          if (qq < ne) inside = inside && (cross_e(Q[qq], x, y) > 0.0);
+      }
+      ins[q] = inside;
+    }
+    // ---- bookkeeping: classes, ballots, farthest candidates ----
+#pragma unroll
+    for (int kk = 0; kk < NCH; ++kk) {
+      const uint32_t cc = kk * CWARPS + warp;
+      if (cc * 64 >= cnt) break;  // warp-uniform
+      uint32_t lw2 = 0, up2 = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = 2 * kk + h;
+        const uint32_t i = first + cc * 64 + 2 * lane + h;
+        const bool keep = pv[q] && !ins[q];
+        noncol = noncol || (pv[q] && cl[q] != 0.0);
+        const bool member = keep && i != p0 && i != pr;
+        const bool lw = member && cl[q] < 0.0;  // hull.cpp:115-117
+        const bool up = member && !(cl[q] < 0.0);
+        lw2 |= (uint32_t)lw << h;
+        up2 |= (uint32_t)up << h;
+        kept += keep;
+        // the candidates only move when d reaches the running maximum
+        const double dl = -cl[q];
+        if (lw && dl > 0.0 && dl >= a0.d) cand_visit(a0, dl, px[q], py[q], pid[q], i, true);
+        if (up && du[q] > 0.0 && du[q] >= a1.d) cand_visit(a1, du[q], px[q], py[q], pid[q], i, false);
+      }
+      const uint32_t le = __ballot_sync(FULL, lw2 & 1u), lodd = __ballot_sync(FULL, lw2 & 2u);
+      const uint32_t ue = __ballot_sync(FULL, up2 & 1u), uodd = __ballot_sync(FULL, up2 & 2u);
       if (lane == 0) B.bits[(first >> 6) + cc] = make_uint4(le, lodd, ue, uodd);
     }
   });

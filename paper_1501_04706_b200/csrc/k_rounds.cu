@@ -39,22 +39,31 @@ SH_DEV Route ldcg_route(const Route* p) {
   return r;
 }
 
-// Route one member (x, y, id) of old segment r,
-// branch-free:
+// Route one member (x, y, id) of old segment s whose Route row is at rp
+// (shared or, with GLOBAL, global memory), SURVEY.md section 7.3:
 //   left = lower ? lex(p) < lex(C) : lex(C) < lex(p)
 //   d    = outward_distance(left ? (A, C) : (C, B), p)   (geometry.hpp:25-27)
 //   keep iff the segment splits, p is not C itself and d > 0 (hull.cpp:199)
-SH_DEV bool route_point(const Route& r, double x, double y, uint32_t id, double& d,
-                        uint32_t& nseg) {
-  const bool lower = r.flags & RT_LOWER;
-  const double ux = lower ? x : r.cx, uy = lower ? y : r.cy;
-  const double vx = lower ? r.cx : x, vy = lower ? r.cy : y;
-  const bool left = lex_less(ux, uy, vx, vy);
-  const double ax = left ? r.ax : r.cx, ay = left ? r.ay : r.cy;
-  const double bx = left ? r.cx : r.bx, by = left ? r.cy : r.by;
-  d = outward_e(make_edge(ax, ay, bx, by), x, y);
-  nseg = r.ns + (left ? 0u : 1u);
-  return (r.flags & RT_SPLIT) && id != r.cid && d > 0.0;
+// The row stores A | C | B as consecutive double2, so the edge endpoints are
+// fetched by computed offset instead of being selected in registers.
+template <bool GLOBAL>
+SH_DEV bool route_point(const Route* rp, double x, double y, uint32_t id, double& d,
+                        uint32_t& nseg, bool& lower) {
+  const double2* row = reinterpret_cast<const double2*>(rp);
+  const double2 C = GLOBAL ? __ldcg(row + 1) : row[1];
+  const uint4 meta = GLOBAL ? __ldcg(reinterpret_cast<const uint4*>(row + 3))
+                            : *reinterpret_cast<const uint4*>(row + 3);  // cid, ns, flags
+  lower = meta.z & RT_LOWER;
+  const bool xeq = x == C.x;
+  const bool lt = x < C.x || (xeq && y < C.y);
+  const bool eq = xeq && y == C.y;
+  const bool left = lower ? lt : !(lt || eq);
+  const int o = left ? 0 : 1;
+  const double2 S = GLOBAL ? __ldcg(row + o) : row[o];
+  const double2 E = GLOBAL ? __ldcg(row + o + 1) : row[o + 1];
+  d = outward_e(make_edge(S.x, S.y, E.x, E.y), x, y);
+  nseg = meta.y + (left ? 0u : 1u);
+  return (meta.z & RT_SPLIT) && id != meta.x && d > 0.0;
 }
 
 // Dense append of this thread's survivors to the CTA's run of the next live
@@ -87,28 +96,15 @@ SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py
   }
 }
 
-// Farthest-point contenders of a CTA with shared-memory slots (small tables).
-//   phase A (tile k): filter on the running maximum, atomicMax on the slot's
-//     distance bits; points that reached the maximum are listed in list k%3
-//   phase B (tile k+1, after the end-of-tile barrier): listed points still at
-//     the slot maximum update the slot record under its lock
-// Lists are triple-buffered so the reset of list (k+1)%3 in tile k never
-// races with a reader or a writer.
-struct CEntry {
-  double d, x, y;
-  uint32_t id, tl;  // tl = slot << 1 | lower
-};
-struct CList {
-  CEntry e[3][CLIST];
-  uint32_t n[3];
-};
-
+// Farthest-point contenders of a CTA with shared-memory slots (small tables):
+// a point that reaches the slot's running maximum (atomicMax on the distance
+// bits) settles the comparator under the record's lock.  After a CTA's first
+// tile almost no point passes the filter, so the lock is rare.
 template <int NP>
-SH_DEV void contend_tile(unsigned long long* s_db, SlotRec* s_rec, CList& L, uint32_t k,
-                         uint32_t keepm, const double (&px)[NP], const double (&py)[NP],
+SH_DEV void contend_tile(unsigned long long* s_db, SlotRec* s_rec, uint32_t keepm,
+                         const double (&px)[NP], const double (&py)[NP],
                          const double (&pd)[NP], const uint32_t (&pid)[NP],
                          const uint32_t (&pseg)[NP], uint32_t lowm) {
-  const uint32_t b = k % 3u;
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
     if ((keepm >> j) & 1u) {
@@ -116,32 +112,11 @@ SH_DEV void contend_tile(unsigned long long* s_db, SlotRec* s_rec, CList& L, uin
       if (db >= *(volatile unsigned long long*)&s_db[pseg[j]]) {
         const unsigned long long old = atomicMax(&s_db[pseg[j]], db);
         if (db >= old) {
-          const uint32_t i = atomicAdd(&L.n[b], 1u);
-          if (i < (uint32_t)CLIST) {
-            CEntry ce;
-            ce.d = pd[j]; ce.x = px[j]; ce.y = py[j]; ce.id = pid[j];
-            ce.tl = (pseg[j] << 1) | ((lowm >> j) & 1u);
-            L.e[b][i] = ce;
-          } else {  // list overflow (adversarial order): resolve right away
-            Cand me;
-            me.d = pd[j]; me.x = px[j]; me.y = py[j]; me.id = pid[j]; me.pos = 0;
-            rec_update<true>(&s_rec[pseg[j]], me, (lowm >> j) & 1u);
-          }
+          Cand me;
+          me.d = pd[j]; me.x = px[j]; me.y = py[j]; me.id = pid[j]; me.pos = 0;
+          rec_update<true>(&s_rec[pseg[j]], me, (lowm >> j) & 1u);
         }
       }
-    }
-  }
-}
-
-SH_DEV void resolve_list(unsigned long long* s_db, SlotRec* s_rec, CList& L, uint32_t b) {
-  const uint32_t cnt = min(*(volatile uint32_t*)&L.n[b], (uint32_t)CLIST);
-  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const CEntry ce = L.e[b][i];
-    const uint32_t t = ce.tl >> 1;
-    if ((unsigned long long)__double_as_longlong(ce.d) == *(volatile unsigned long long*)&s_db[t]) {
-      Cand me;
-      me.d = ce.d; me.x = ce.x; me.y = ce.y; me.id = ce.id; me.pos = 0;
-      rec_update<true>(&s_rec[t], me, ce.tl & 1u);
     }
   }
 }
@@ -173,13 +148,13 @@ SH_DEV uint32_t sum_runs(const uint32_t* cnt, uint32_t nruns, uint32_t* s_ws) {
 // ===========================================================================
 
 constexpr int K3_NS = STREAM_NS;
-constexpr int K3_NP = 2 * (STREAM_T / 64 / SWARPS);   // points per thread per tile
+constexpr int K3_NP = 2 * (STREAM_T / 64 / CWARPS);   // points per consumer thread per tile
 
 template <bool IDS>
 struct K3Layout {
   using Ring = TileRing<STREAM_T, K3_NS, IDS, 16>;
   static constexpr size_t kRing = (Ring::kBytes + 127) / 128 * 128;
-  static constexpr size_t kBytes = kRing + sizeof(CList);
+  static constexpr size_t kBytes = kRing;
 };
 
 template <bool IDS>
@@ -188,7 +163,6 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
   using L = K3Layout<IDS>;
   typename L::Ring R;
   R.carve(smem_raw);
-  CList& cl = *reinterpret_cast<CList*>(smem_raw + L::kRing);
   __shared__ Route s_rt[2];
   __shared__ unsigned long long s_db[4];
   __shared__ SlotRec s_rec[4];
@@ -240,23 +214,18 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
     s_Slon = Slon;
     s_off = 0;
     for (int t = 0; t < 4; ++t) rec_clear(&s_db[t], &s_rec[t]);
-    for (int b = 0; b < 3; ++b) cl.n[b] = 0;
     if (blockIdx.x == 0)  // clear round 2's slots
       for (int t = 0; t < 8; ++t) rec_clear(&B.Sd[2][t], &B.Srec[2][t]);
   }
   __syncthreads();
-  const Route rlo = s_rt[0], rup = s_rt[1];
   const uint32_t Sn = s_Sn, Slon = s_Slon;
   const uint32_t run_base = blockIdx.x * B.run_q;
   double2* Oxy = B.Lxy[1];
   uint2* Ois = B.Lis[1];
-  uint32_t k = 0;
 
   // ---- point phase: forward over the input (K2 left the head in L2) ----
   stream_input(R, n, X, Y, I, reinterpret_cast<const unsigned char*>(B.bits), false,
                [&](int s, uint32_t first, uint32_t cnt) {
-    if (k) resolve_list(s_db, s_rec, cl, (k - 1) % 3u);
-    if (threadIdx.x == 0) cl.n[(k + 1) % 3u] = 0;
     const double* xs = R.xs + s * STREAM_T;
     const double* ys = R.ys + s * STREAM_T;
     const uint32_t* is = R.is + s * STREAM_T;
@@ -267,7 +236,7 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
     uint32_t keepm = 0, lowm = 0;
 #pragma unroll
     for (int kk = 0; kk < K3_NP / 2; ++kk) {
-      const uint32_t cc = kk * SWARPS + warp;  // chunk of 64 points within the tile
+      const uint32_t cc = kk * CWARPS + warp;  // chunk of 64 points within the tile
       const uint32_t j = cc * 64 + 2 * lane;
       uint4 bits = make_uint4(0u, 0u, 0u, 0u);
       double2 xv = make_double2(0.0, 0.0), yv = xv;
@@ -298,19 +267,22 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
         pid[q] = IDS ? (h ? iv.y : iv.x) : first + j + h;
         const uint32_t lw = ((h ? bits.y : bits.x) >> lane) & 1u;
         const uint32_t uw = ((h ? bits.w : bits.z) >> lane) & 1u;
-        const bool keep = route_point(lw ? rlo : rup, px[q], py[q], pid[q], pd[q], pseg[q]);
-        if ((lw | uw) && keep) keepm |= 1u << q;
+        bool lower = false;
+        if ((lw | uw) && route_point<false>(s_rt + (lw ? 0 : 1), px[q], py[q], pid[q], pd[q], pseg[q], lower))
+          keepm |= 1u << q;
         if (lw) lowm |= 1u << q;
       }
     }
-    contend_tile<K3_NP>(s_db, s_rec, cl, k, keepm, px, py, pd, pid, pseg, lowm);
+    contend_tile<K3_NP>(s_db, s_rec, keepm, px, py, pd, pid, pseg, lowm);
     run_append<K3_NP>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, run_base);
-    ++k;
   });
-  if (k) resolve_list(s_db, s_rec, cl, (k - 1) % 3u);
 
   // ---- flush the CTA's records to the global slots of round 2's argmax ----
   __syncthreads();
+  if (threadIdx.x == 0 && (s_off & 1u)) {  // pad the run to an even length
+    Oxy[run_base + s_off] = make_double2(0.0, 0.0);
+    Ois[run_base + s_off] = make_uint2(NONE, NONE);
+  }
   flush_slots(s_db, s_rec, Sn, Slon, B.Sd[1], B.Srec[1]);
   if (threadIdx.x == 0) B.run_cnt[1][blockIdx.x] = s_off;
 
@@ -331,6 +303,8 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
   st.points_removed = before - (Sn + mn);
   st.pad = 0;
   st.end_ns = globaltimer_ns() - *(volatile unsigned long long*)&c->t0_ns;
+  st.table_ns = 0;
+  st.points_ns = 0;
   B.stats[0] = st;
   c->round = 1;
   c->S_cur = Sn;
@@ -346,14 +320,16 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
 // ===========================================================================
 
 constexpr int RW = RTPB / 32;          // warps per CTA
-constexpr int KR_U = 4;                // live points per thread per tile
-constexpr int KR_TILE = RTPB * KR_U;   // 2048
+constexpr int KR_U = LIVE_T / CTHREADS;  // live points per consumer thread per tile
 
 struct RoundSmem {
-  Route rt[SMALL_S];               // route entries of a small table     64 KB
-  unsigned long long db[NSLOT];    // CTA farthest slots: distance bits   16 KB
-  SlotRec rec[NSLOT];              //                     records         64 KB
-  CList cl;                        // phase-B contender lists             24 KB
+  double2 lxy[LIVE_NS][LIVE_T];    // TMA ring of live points: xy          64 KB
+  uint2 lis[LIVE_NS][LIVE_T];      //                          (id, seg)   32 KB
+  unsigned long long lbar[LIVE_NS];   // full
+  unsigned long long lebar[LIVE_NS];  // empty (one arrival per warp)
+  Route rt[SMALL_S];               // route entries of a small table       32 KB
+  unsigned long long db[NSLOT];    // CTA farthest slots: distance bits     8 KB
+  SlotRec rec[NSLOT];              //                     records          32 KB
 };
 
 // Barrier over the CTAs still working on the rounds.
@@ -509,7 +485,7 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   return true;
 }
 
-constexpr uint32_t ROUND_TARGET = 8192;  // live points per active CTA before CTAs retire
+constexpr uint32_t ROUND_TARGET = 2 * LIVE_T;  // live points per active CTA before CTAs retire
 
 __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -528,6 +504,16 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   const uint32_t target = min(ROUND_TARGET, q);
   uint32_t P = gridDim.x;
   bool recs_smem = false;  // this round's input records live in this CTA's smem
+  uint32_t kbase = 0;      // live tiles this CTA consumed in earlier rounds
+  unsigned long long t_table = 0, t_points = 0;  // CTA 0 phase timestamps
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < LIVE_NS; ++i) {
+      mbar_init(&sm.lbar[i], 1);
+      mbar_init(&sm.lebar[i], CWARPS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
 
   while (true) {
     // active CTAs for this round: ~ROUND_TARGET live points each (m only
@@ -548,6 +534,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     } else if (!table_large(B, S, Slo, pin, pout, sin, sout, P, s_ws, Sn, Slon)) {
       return;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) t_table = globaltimer_ns();
     // clear round r+1's global farthest slots (at most 2 Sn segments) when
     // round r+1 will use a small table; a large table clears its own slots
     if (Sn <= (uint32_t)SMALL_S) {
@@ -560,7 +547,8 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       uint32_t tot;
       for (uint32_t j0 = 0; j0 < nruns; j0 += RTPB) {
         const uint32_t j = j0 + threadIdx.x;
-        const uint32_t v = j < nruns ? (nruns == 1 ? m : __ldcg(B.run_cnt[pin] + j)) : 0u;
+        uint32_t v = j < nruns ? (nruns == 1 ? m : __ldcg(B.run_cnt[pin] + j)) : 0u;
+        v += v & 1u;  // runs are padded to even lengths
         const uint32_t base0 = j0 ? s_pref[j0] : 0u;
         const uint32_t ex = block_exclusive_scan(v, s_ws, &tot);
         if (j < nruns) s_pref[j] = base0 + ex;
@@ -568,13 +556,12 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
         __syncthreads();
       }
     }
-    if (threadIdx.x == 0) {
-      s_off = 0;
-      for (int b = 0; b < 3; ++b) sm.cl.n[b] = 0;
-    }
+    if (threadIdx.x == 0) s_off = 0;
     __syncthreads();
 
     // ---- point phase: virtual range [lo, hi) of the live set -> run j ----
+    // The runs are read as one virtual range (padded counts, all even); each
+    // tile of LIVE_T positions is fetched by bulk copies, one per run piece.
     const double2* Ixy = B.Lxy[pin];
     const uint2* Iis = B.Lis[pin];
     double2* Oxy = B.Lxy[pout];
@@ -582,75 +569,137 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     unsigned long long* Sd = B.Sd[sout];
     SlotRec* Srec = B.Srec[sout];
     const uint32_t obase = blockIdx.x * q;
-    const uint32_t lo = (uint32_t)((unsigned long long)m * blockIdx.x / P);
-    const uint32_t hi = (uint32_t)((unsigned long long)m * (blockIdx.x + 1) / P);
-    uint32_t k = 0;
-    for (uint32_t t0 = lo; t0 < hi; t0 += KR_TILE) {
-      if (small && k) resolve_list(sm.db, sm.rec, sm.cl, (k - 1) % 3u);
-      if (small && threadIdx.x == 0) sm.cl.n[(k + 1) % 3u] = 0;
-      // run containing the tile start (binary search; points walk forward)
-      uint32_t rb = 0;
-      {
-        uint32_t a0 = 0, a1 = nruns;
-        while (a1 - a0 > 1) {
-          const uint32_t mid = (a0 + a1) >> 1;
-          if (s_pref[mid] <= t0) a0 = mid; else a1 = mid;
-        }
-        rb = a0;
+    const uint32_t Mp = s_pref[nruns];
+    const uint32_t lo = 2u * (uint32_t)((unsigned long long)(Mp / 2) * blockIdx.x / P);
+    const uint32_t hi = 2u * (uint32_t)((unsigned long long)(Mp / 2) * (blockIdx.x + 1) / P);
+    const uint32_t ntl = (hi - lo + LIVE_T - 1) / LIVE_T;
+    // ring stages/phases continue across rounds: tile kk of this round is
+    // the CTA's (kbase + kk)-th tile overall.  Fragmented live sets (short
+    // runs: many tiny bulk copies, each ~70 ns to issue) are read with plain
+    // loads by the consumers instead.
+    const bool use_tma = Mp >= 256u * nruns;
+    auto issue = [&](uint32_t kk) {  // producer lane
+      const int st = (int)((kbase + kk) % LIVE_NS);
+      const uint32_t t0 = lo + kk * LIVE_T, t1 = min(hi, t0 + LIVE_T);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&sm.lbar[st], (t1 - t0) * 24u);
+      uint32_t a0 = 0, a1 = nruns;
+      while (a1 - a0 > 1) {
+        const uint32_t mid = (a0 + a1) >> 1;
+        if (s_pref[mid] <= t0) a0 = mid; else a1 = mid;
       }
-      double px[KR_U], py[KR_U], pd[KR_U];
-      uint32_t pid[KR_U], pseg[KR_U], oseg[KR_U];
-      uint32_t keepm = 0, lowm = 0;
-#pragma unroll
-      for (int u = 0; u < KR_U; ++u) {
-        const uint32_t e = t0 + u * RTPB + threadIdx.x;
-        px[u] = py[u] = 0.0;
-        pid[u] = 0;
-        oseg[u] = NONE;
-        if (e < hi) {
-          uint32_t b2 = rb;
-          while (e >= s_pref[b2 + 1]) ++b2;
-          const uint32_t ph = b2 * q + (e - s_pref[b2]);
-          const double2 v = __ldcg(Ixy + ph);
-          const uint2 is = __ldcg(Iis + ph);
-          px[u] = v.x;
-          py[u] = v.y;
-          pid[u] = is.x;
-          oseg[u] = is.y;
-        }
+      for (uint32_t pos = t0, rb = a0; pos < t1; ++rb) {
+        const uint32_t end = min(t1, s_pref[rb + 1]);
+        if (end <= pos) continue;
+        const uint32_t ph = rb * q + (pos - s_pref[rb]);
+        tma_load_1d(&sm.lxy[st][pos - t0], Ixy + ph, (end - pos) * 16u, &sm.lbar[st]);
+        tma_load_1d(&sm.lis[st][pos - t0], Iis + ph, (end - pos) * 8u, &sm.lbar[st]);
+        pos = end;
       }
-#pragma unroll
-      for (int u = 0; u < KR_U; ++u) {
-        pd[u] = 0.0;
-        pseg[u] = 0;
-        if (oseg[u] != NONE) {
-          const Route rr = small ? sm.rt[oseg[u]] : ldcg_route(B.route + oseg[u]);
-          if (route_point(rr, px[u], py[u], pid[u], pd[u], pseg[u])) keepm |= 1u << u;
-          if (rr.flags & RT_LOWER) lowm |= 1u << u;
+    };
+    const int wid = threadIdx.x >> 5;
+    if (wid == CWARPS) {  // producer warp
+      if (use_tma && (threadIdx.x & 31) == 0) {
+        for (uint32_t kk = 0; kk < ntl; ++kk) {
+          const uint32_t g = kbase + kk;
+          if (kk >= (uint32_t)LIVE_NS) mbar_wait(&sm.lebar[g % LIVE_NS], ((g / LIVE_NS) - 1) & 1u);
+          issue(kk);
         }
       }
-      if (small) {
-        contend_tile<KR_U>(sm.db, sm.rec, sm.cl, k, keepm, px, py, pd, pid, pseg, lowm);
-      } else {
-        // large table: fire-and-forget max of the distance bits; the winners
-        // are identified after the barrier (winner pass below)
+    } else {
+      for (uint32_t k = 0; k < ntl; ++k) {
+        const int st = (int)((kbase + k) % LIVE_NS);
+        const uint32_t ph = ((kbase + k) / LIVE_NS) & 1u;
+        const uint32_t t0 = lo + k * LIVE_T, tc = min(hi, t0 + LIVE_T) - t0;
+        double px[KR_U], py[KR_U], pd[KR_U];
+        uint32_t pid[KR_U], pseg[KR_U], oseg[KR_U];
+        uint32_t keepm = 0, lowm = 0;
+        if (use_tma) {
+          mbar_wait(&sm.lbar[st], ph);
 #pragma unroll
-        for (int u = 0; u < KR_U; ++u)
-          if ((keepm >> u) & 1u)
-            atomicMax(Sd + pseg[u], (unsigned long long)__double_as_longlong(pd[u]));
+          for (int u = 0; u < KR_U; ++u) {
+            const uint32_t e = u * CTHREADS + threadIdx.x;
+            px[u] = py[u] = 0.0;
+            pid[u] = 0;
+            oseg[u] = NONE;
+            if (e < tc) {
+              const double2 v = sm.lxy[st][e];
+              const uint2 is = sm.lis[st][e];
+              px[u] = v.x;
+              py[u] = v.y;
+              pid[u] = is.x;
+              oseg[u] = is.y;  // NONE for the pad entry of an odd run
+            }
+          }
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.lebar[st]);  // stage read
+        } else {
+          uint32_t rb = 0;
+          {
+            uint32_t a0 = 0, a1 = nruns;
+            while (a1 - a0 > 1) {
+              const uint32_t mid = (a0 + a1) >> 1;
+              if (s_pref[mid] <= t0) a0 = mid; else a1 = mid;
+            }
+            rb = a0;
+          }
+#pragma unroll
+          for (int u = 0; u < KR_U; ++u) {
+            const uint32_t e = u * CTHREADS + threadIdx.x;
+            px[u] = py[u] = 0.0;
+            pid[u] = 0;
+            oseg[u] = NONE;
+            if (e < tc) {
+              const uint32_t v0 = t0 + e;
+              uint32_t b2 = rb;
+              while (v0 >= s_pref[b2 + 1]) ++b2;
+              const uint32_t phys = b2 * q + (v0 - s_pref[b2]);
+              const double2 v = __ldcg(Ixy + phys);
+              const uint2 is = __ldcg(Iis + phys);
+              px[u] = v.x;
+              py[u] = v.y;
+              pid[u] = is.x;
+              oseg[u] = is.y;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < KR_U; ++u) {
+          pd[u] = 0.0;
+          pseg[u] = 0;
+          if (oseg[u] != NONE) {
+            bool lower = false;
+            const bool keep = small ? route_point<false>(sm.rt + oseg[u], px[u], py[u], pid[u], pd[u], pseg[u], lower)
+                                    : route_point<true>(B.route + oseg[u], px[u], py[u], pid[u], pd[u], pseg[u], lower);
+            if (keep) keepm |= 1u << u;
+            if (lower) lowm |= 1u << u;
+          }
+        }
+        if (small) {
+          contend_tile<KR_U>(sm.db, sm.rec, keepm, px, py, pd, pid, pseg, lowm);
+        } else {
+          // large table: fire-and-forget max of the distance bits; the winners
+          // are identified after the barrier (winner pass below)
+#pragma unroll
+          for (int u = 0; u < KR_U; ++u)
+            if ((keepm >> u) & 1u)
+              atomicMax(Sd + pseg[u], (unsigned long long)__double_as_longlong(pd[u]));
+        }
+        run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase);
       }
-      run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase);
-      __syncthreads();
-      ++k;
+    }
+    __syncthreads();
+    if (use_tma) kbase += ntl;  // stage uses so far (phase parity of the ring)
+    if (threadIdx.x == 0 && (s_off & 1u)) {  // pad the run to an even length
+      Oxy[obase + s_off] = make_double2(0.0, 0.0);
+      Ois[obase + s_off] = make_uint2(NONE, NONE);
     }
     // a lone CTA whose next table is small keeps its records in smem
     const bool keep_smem = small && P == 1 && Sn <= (uint32_t)SMALL_S;
-    if (small) {
-      if (k) resolve_list(sm.db, sm.rec, sm.cl, (k - 1) % 3u);
-      __syncthreads();
-      if (!keep_smem) flush_slots(sm.db, sm.rec, Sn, Slon, Sd, Srec);
-    }
+    if (small && !keep_smem) flush_slots(sm.db, sm.rec, Sn, Slon, Sd, Srec);
     if (threadIdx.x == 0) B.run_cnt[pout][blockIdx.x] = s_off;
+    if (blockIdx.x == 0 && threadIdx.x == 0) t_points = globaltimer_ns();
+    if (threadIdx.x == 0 && r == c->tl_round) B.dbg[blockIdx.x] = globaltimer_ns() - c->t0_ns;
     rounds_barrier(c, P);
     if (!small) {
       // winner pass: every survivor of this CTA (its run, still hot in L2)
@@ -683,7 +732,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       st.points_remaining = Sn + mn;
       st.points_removed = (S + m) - (Sn + mn);
       st.pad = 0;
-      st.end_ns = globaltimer_ns() - *(volatile unsigned long long*)&c->t0_ns;
+      const unsigned long long t0 = *(volatile unsigned long long*)&c->t0_ns;
+      st.end_ns = globaltimer_ns() - t0;
+      st.table_ns = t_table - t0;
+      st.points_ns = t_points - t0;
       B.stats[r - 1] = st;
     }
     S = Sn;

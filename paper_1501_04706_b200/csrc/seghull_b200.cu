@@ -63,6 +63,9 @@ struct DeviceInfo {
 };
 
 std::mutex g_mutex;
+int g_trace_round = 0;                          // debug: trace CTA 0's tiles of this round
+thread_local unsigned long long g_last_tl[33];  // debug: [0] = count, then timestamps
+thread_local std::vector<unsigned long long> g_last_ctas;  // debug: per-CTA point-phase ends
 std::vector<DeviceInfo> g_dev;
 
 struct Workspace {
@@ -148,6 +151,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   const size_t o_k1 = take(sizeof(K1Partial) * ws->stream_grid);
   const size_t o_stats = take(sizeof(StatRec) * STATS_CAP);
   const size_t o_blk = take(sizeof(uint32_t) * 2 * MAX_ROUND_BLOCKS);
+  const size_t o_dbg = take(sizeof(unsigned long long) * MAX_ROUND_BLOCKS);
   const size_t o_tiles = take(sizeof(unsigned long long) * ws->tiles_cap);
   const size_t o_bits = take(sizeof(uint4) * ((N + 63) / 64));
   size_t o_lxy[2], o_lis[2], o_rc[2], o_tx[2], o_ty[2], o_tid[2], o_sd[3], o_sw[3];
@@ -180,6 +184,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   B.k1part = (K1Partial*)(a + o_k1);
   B.stats = (StatRec*)(a + o_stats);
   B.blk_cnt = (uint32_t*)(a + o_blk);
+  B.dbg = (unsigned long long*)(a + o_dbg);
   B.tile_status = (unsigned long long*)(a + o_tiles);
   B.bits = (uint4*)(a + o_bits);
   for (int p = 0; p < 2; ++p) {
@@ -301,6 +306,11 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
 
   // a zeroed control block is the initial state (ST_RUNNING == 0)
   CK(cudaMemsetAsync(B.ctl, 0, sizeof(Ctl), st));
+  if (g_trace_round) {
+    const uint32_t tr = (uint32_t)g_trace_round;
+    CK(cudaMemcpyAsync(&B.ctl->tl_round, &tr, sizeof(tr), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
 
   const uint64_t ntiles = (n + STREAM_T - 1) / STREAM_T;
   const int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ws.stream_grid));
@@ -331,6 +341,13 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   CK(cudaStreamSynchronize(st));
 
   const Ctl& c = *ws.h_ctl;
+  g_last_tl[0] = c.tl_n;
+  for (uint32_t i = 0; i < c.tl_n && i < 32; ++i) g_last_tl[i + 1] = c.tl[i];
+  if (g_trace_round) {
+    g_last_ctas.resize(MAX_ROUND_BLOCKS);
+    CK(cudaMemcpy(g_last_ctas.data(), B.dbg, sizeof(unsigned long long) * MAX_ROUND_BLOCKS,
+                  cudaMemcpyDeviceToHost));
+  }
   out.rounds = c.round;
   out.kept = rq.mode == SH_MODE_WITH_PREPROCESS ? c.kept : n;
   out.bad = c.bad_index;
@@ -476,6 +493,8 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
       res->stats[i].points_remaining = ws->h_stats[i].points_remaining;
       res->stats[i].points_removed = ws->h_stats[i].points_removed;
       res->stats[i].end_ns = ws->h_stats[i].end_ns;
+      res->stats[i].table_ns = ws->h_stats[i].table_ns;
+      res->stats[i].points_ns = ws->h_stats[i].points_ns;
     }
     if (timings) {
       auto el = [&](int i, int j) {
@@ -519,6 +538,20 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
 extern "C" {
 
 int sh_b200_abi_version(void) { return SH_B200_ABI_VERSION; }
+
+// Debug aid (not part of include/seghull_b200.h): trace CTA 0's tile waits
+// in round `r` of subsequent calls; read them back after a call.
+void sh_b200_debug_trace_round(int r) { g_trace_round = r; }
+int sh_b200_debug_last_ctas(unsigned long long* out, int cap) {
+  const int n = (int)g_last_ctas.size();
+  for (int i = 0; i < n && i < cap; ++i) out[i] = g_last_ctas[i];
+  return n;
+}
+int sh_b200_debug_last_timeline(unsigned long long* out, int cap) {
+  const int n = (int)g_last_tl[0];
+  for (int i = 0; i < n && i < cap; ++i) out[i] = g_last_tl[i + 1];
+  return n;
+}
 
 int sh_b200_hull_ex(const sh_hull_request* req, sh_hull_result* res) { return hull_impl(req, res); }
 

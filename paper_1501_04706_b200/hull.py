@@ -133,6 +133,7 @@ class HullResult:
     kernel_launches: int = 0
     kernels: object = None
     round_end_ms: list = field(default_factory=list)  # device time at the end of each round
+    round_phases_ms: list = field(default_factory=list)  # (table end, points end, round end)
 
     @property
     def vertices(self) -> list:
@@ -224,12 +225,14 @@ def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, st
     sts = [SegmentStats(int(st[i].iteration), int(st[i].segments), int(st[i].points_remaining),
                         int(st[i].points_removed)) for i in range(nst)]
     ends = [st[i].end_ns * 1e-6 for i in range(nst)]
+    phases = [(st[i].table_ns * 1e-6, st[i].points_ns * 1e-6, st[i].end_ns * 1e-6)
+              for i in range(nst)]
     ph = PhaseTimings(res.phases.pre_ms, res.phases.split_ms, res.phases.recurse_ms,
                       res.phases.total_ms)
     k = res.kernels
     kt = KernelTimings(k.h2d_ms, k.extremes_ms, k.filter_ms, k.first_round_ms, k.rounds_ms,
                        k.d2h_ms)
-    return res, sts, ph, kt, ends
+    return res, sts, ph, kt, (ends, phases)
 
 
 def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int | None = None,
@@ -255,7 +258,7 @@ def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int |
     r = HullResult(ox[:h].copy(), oy[:h].copy(), oi[:h].copy(), sts, ph, int(res.kept),
                    int(res.rounds), int(res.kernel_launches))
     r.kernels = kt
-    r.round_end_ms = ends
+    r.round_end_ms, r.round_phases_ms = ends
     return r
 
 
@@ -273,6 +276,7 @@ class DeviceHull:
     rounds: int
     kernel_launches: int
     round_end_ms: list = field(default_factory=list)
+    round_phases_ms: list = field(default_factory=list)
 
 
 def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int | None = None,
@@ -299,7 +303,7 @@ def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int |
                              int(ox.shape[0]), (1 << 16) if stats else 0)
     h = int(res.h)
     return DeviceHull(ox[:h], oy[:h], oi[:h], h, sts, ph, kt, int(res.kept), int(res.rounds),
-                      int(res.kernel_launches), ends)
+                      int(res.kernel_launches), ends[0], ends[1])
 
 
 def run(points: PointSet, mode: Mode = Mode.WithPreprocess,

@@ -80,6 +80,6 @@ def test_host_generators_bit_identical_to_reference_stream():
 
 
 def test_struct_layouts_match_header():
-    assert ctypes.sizeof(_lib.sh_round_stat) == 40
+    assert ctypes.sizeof(_lib.sh_round_stat) == 56
     assert ctypes.sizeof(_lib.sh_phase_ms) == 32
     assert ctypes.sizeof(_lib.sh_hull_request) == 56

@@ -18,7 +18,30 @@ else:
     hx, hy = dataio.gen_circle(n, 1)
     x, y = torch.from_numpy(hx).cuda(), torch.from_numpy(hy).cuda()
 torch.cuda.synchronize()
+trace = int(os.environ.get("TRACE_ROUND", "0"))
+if trace:
+    import ctypes
+    from paper_1501_04706_b200 import _lib
+    L = _lib.load()
+    L.sh_b200_debug_trace_round(trace)
 for _ in range(reps):
     r = hull.run_device(x, y, 1, timings=True)
     print(kind, n, "h", r.h, "rounds", r.rounds, r.kernels, r.phase_timings, flush=True)
     print("   round end (ms since K1 start):", [round(t, 4) for t in r.round_end_ms], flush=True)
+    prev = 0.0
+    for i, (ta, tp, te) in enumerate(r.round_phases_ms):
+        if ta:
+            print(f"   round {i+1}: table {1e3*(ta-prev):7.1f} us  points {1e3*(tp-ta):7.1f} us  close {1e3*(te-tp):7.1f} us", flush=True)
+        prev = te
+    if trace:
+        buf = (ctypes.c_ulonglong * 32)()
+        k = L.sh_b200_debug_last_timeline(buf, 32)
+        ts = [buf[i] / 1e3 for i in range(k)]
+        print(f"   trace round {trace} (us since K1 start; tile wait begin/end):", [round(t, 2) for t in ts])
+        cb = (ctypes.c_ulonglong * 1024)()
+        L.sh_b200_debug_last_ctas(cb, 1024)
+        ends = sorted(cb[i] / 1e3 for i in range(1024) if cb[i])
+        if ends:
+            import statistics
+            print(f"   CTA point-phase ends: n={len(ends)} min {ends[0]:.1f} median {statistics.median(ends):.1f} max {ends[-1]:.1f} us; deciles",
+                  [round(ends[int(len(ends) * d / 10)], 1) for d in range(10)])
