@@ -312,28 +312,15 @@ def run_b200(a):
            torch.empty(cap, dtype=torch.int64, device=dev))
     launches = [0]
 
+    from paper_1501_04706_b200 import shard
+
     def merge(dh):
         """all-gather the shard hulls (NCCL over NVLink) and hull them on every rank."""
-        cnt = torch.tensor([dh.h], dtype=torch.int64, device=dev)
-        cnts = torch.empty(world, dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(cnts, cnt)
-        hmax = int(cnts.max().item())
-        buf = torch.empty((3, hmax), dtype=torch.float64, device=dev)
-        # pad with copies of vertex 0 (duplicates leave the hull unchanged and
-        # carry the same global id, so canonical indices are unaffected)
-        buf[0, :dh.h] = dh.x
-        buf[1, :dh.h] = dh.y
-        buf[2, :dh.h] = (dh.indices + first).to(torch.float64)
-        if dh.h < hmax:
-            buf[:, dh.h:] = buf[:, :1]
-        allb = torch.empty((world, 3, hmax), dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(allb, buf)
-        mx = allb[:, 0, :].reshape(-1).contiguous()
-        my = allb[:, 1, :].reshape(-1).contiguous()
-        mid = allb[:, 2, :].reshape(-1).to(torch.int64).to(torch.int32).contiguous()
-        m = hull.run_device(mx, my, a.mode, ids=mid, stream=sp, stats=False)
-        launches[0] += m.kernel_launches
-        return m
+        def hull_with_ids(mx, my, mids):
+            m = hull.run_device(mx, my, a.mode, ids=mids, stream=sp, stats=False)
+            launches[0] += m.kernel_launches
+            return m
+        return shard.merged_hull(dh, first, world, dist.all_gather_into_tensor, hull_with_ids)
 
     def step(timings=False):
         dh = hull.run_device(x, y, a.mode, stream=sp, timings=timings, out=out)
@@ -397,10 +384,11 @@ def run_b200(a):
     bytes_dom, ms_dom = kern[dom]
     achieved = bytes_dom / (ms_dom * 1e-3) / 1e9
     traffic = None
-    try:
+    try:  # DRAM bytes of the same kernel from one ncu --set full capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        traffic = tr.get(a.workload, {}).get(dom)
+        t = tr.get(a.workload, {}).get(dom)
+        traffic = t["dram_bytes"] if t else None
     except Exception:
         pass
     per_kernel = {k: {"ms": round(v[1], 5), "alg_bytes": v[0],
