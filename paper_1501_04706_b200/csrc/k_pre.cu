@@ -350,7 +350,14 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
   Cand a0 = empty_cand(), a1 = empty_cand();
   uint32_t kept = 0;
   bool noncol = false;
-  if (threadIdx.x == 0) R.init();
+  // CTA-wide running maxima of the two chains' distances (positive doubles
+  // order like their bits): a point below them cannot be the CTA's farthest,
+  // so the per-point candidate branch is almost never taken
+  __shared__ unsigned long long s_dmax[2];
+  if (threadIdx.x == 0) {
+    R.init();
+    s_dmax[0] = s_dmax[1] = 0ull;
+  }
   __syncthreads();
 
   // With 4 distinct corners, edge q starts at corner q (left, bottom, right,
@@ -433,6 +440,9 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
       ins[q] = inside;
     }
     // ---- bookkeeping: classes, ballots, farthest candidates ----
+    const double m0 = fmax(a0.d, __longlong_as_double(*(volatile long long*)&s_dmax[0]));
+    const double m1 = fmax(a1.d, __longlong_as_double(*(volatile long long*)&s_dmax[1]));
+    const double ad0 = a0.d, ad1 = a1.d;
 #pragma unroll
     for (int kk = 0; kk < NCH; ++kk) {
       const uint32_t cc = kk * CWARPS + warp;
@@ -452,13 +462,16 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
         kept += keep;
         // the candidates only move when d reaches the running maximum
         const double dl = -cl[q];
-        if (lw && dl > 0.0 && dl >= a0.d) cand_visit(a0, dl, px[q], py[q], pid[q], i, true);
-        if (up && du[q] > 0.0 && du[q] >= a1.d) cand_visit(a1, du[q], px[q], py[q], pid[q], i, false);
+        if (lw && dl > 0.0 && dl >= m0) cand_visit(a0, dl, px[q], py[q], pid[q], i, true);
+        if (up && du[q] > 0.0 && du[q] >= m1) cand_visit(a1, du[q], px[q], py[q], pid[q], i, false);
       }
       const uint32_t le = __ballot_sync(FULL, lw2 & 1u), lodd = __ballot_sync(FULL, lw2 & 2u);
       const uint32_t ue = __ballot_sync(FULL, up2 & 1u), uodd = __ballot_sync(FULL, up2 & 2u);
       if (lane == 0) B.bits[(first >> 6) + cc] = make_uint4(le, lodd, ue, uodd);
     }
+    // publish improvements of this thread's candidates as CTA thresholds
+    if (a0.d > ad0) atomicMax(&s_dmax[0], (unsigned long long)__double_as_longlong(a0.d));
+    if (a1.d > ad1) atomicMax(&s_dmax[1], (unsigned long long)__double_as_longlong(a1.d));
   });
 
   // block reduction of the two chains' farthest candidates
