@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import threading
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -199,6 +200,18 @@ def _prepare(x, y, ids):
     return x, y, ids, px, py, dx, n
 
 
+_tls = threading.local()
+
+
+def _stats_buffer(cap: int):
+    """Per-thread reusable stats array (the library writes min(rounds, cap) rows)."""
+    buf = getattr(_tls, "stats", None)
+    if buf is None or len(buf) < cap:
+        buf = (_lib.sh_round_stat * max(cap, 64))()
+        _tls.stats = buf
+    return buf
+
+
 def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, stats_cap):
     L = _lib.load()
     req = _lib.sh_hull_request()
@@ -210,7 +223,7 @@ def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, st
     req.flags = flags
     req.device = int(device)
     req.stream = stream
-    st = (_lib.sh_round_stat * max(stats_cap, 1))()
+    st = _stats_buffer(stats_cap)
     res = _lib.sh_hull_result()
     res.idx = oi
     res.x = ox
