@@ -141,6 +141,11 @@ SH_DEV unsigned long long globaltimer_ns() {
   return t;
 }
 
+// Programmatic dependent launch (sm_90+): the next kernel in the stream may be
+// scheduled now / this kernel waits for its predecessor's completion + memory.
+SH_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+SH_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 SH_DEV uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

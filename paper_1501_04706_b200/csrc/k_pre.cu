@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
   e[3].x = INF;  e[3].y = -INF;  // top
   for (int k = 0; k < 4; ++k) e[k].id = e[k].pos = NONE;
   unsigned long long bad = ~0ull;
+  pdl_launch_dependents();  // K2 may be scheduled on SMs this kernel frees
   if (blockIdx.x == 0 && threadIdx.x == 0) c->t0_ns = globaltimer_ns();
   // CTA-wide thresholds for the branch-free filter: a point can only become
   // an extreme if it is at least as extreme as the CTA's running extreme
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
   // round-0 farthest slots (K2 offers into Slot[0]; hull_kernels.cuh)
   rec_clear(&B.Sd[0][0], &B.Srec[0][0]);
   rec_clear(&B.Sd[0][1], &B.Srec[0][1]);
+  c->mark[0] = globaltimer_ns() - c->t0_ns;
   if (bad != ~0ull) {
     c->status = ST_NONFINITE;
     return;
@@ -306,6 +308,7 @@ __global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
     for (int j = 0; j < 4; ++j) c->edges[k][j] = 0.0;
   c->distinct = distinct;
   c->nedges = ne;
+  c->mark[0] = globaltimer_ns() - c->t0_ns;
 }
 
 // ===========================================================================
@@ -327,7 +330,10 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
   TileRing<STREAM_T, STREAM_NS, IDS> R;
   R.carve(smem_raw);
   Ctl* c = B.ctl;
+  pdl_wait();               // K1's extremes are complete and visible
+  pdl_launch_dependents();  // K3 may be scheduled on SMs this kernel frees
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) c->mark[1] = globaltimer_ns() - c->t0_ns;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n = B.n;
   const double* __restrict__ X = B.in_x;
@@ -532,6 +538,7 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
     c->round = 0;
     if (kept_all == 2) c->status = ST_DONE;
   }
+  c->mark[2] = globaltimer_ns() - c->t0_ns;
   __threadfence();
 }
 
@@ -561,13 +568,38 @@ void launch_k1(const Bufs& B, bool ids, int grid, cudaStream_t s) {
   else k1_extremes<false><<<grid, STPB, Ring::kBytes, s>>>(B);
 }
 
+// launch with programmatic stream serialization (PDL): the kernel's own
+// griddepcontrol.wait orders it after its predecessor
+template <class K>
+static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaStream_t s,
+                              const Bufs& B, bool cooperative = false) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  if (cooperative) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kernel, B);
+}
+
 void launch_k2(const Bufs& B, bool filter, bool ids, int grid, cudaStream_t s) {
   if (filter) {
-    if (ids) k2_classify<true, true><<<grid, STPB, RingI::kBytes, s>>>(B);
-    else k2_classify<true, false><<<grid, STPB, Ring::kBytes, s>>>(B);
+    if (ids) launch_pdl(k2_classify<true, true>, grid, STPB, RingI::kBytes, s, B);
+    else launch_pdl(k2_classify<true, false>, grid, STPB, Ring::kBytes, s, B);
   } else {
-    if (ids) k2_classify<false, true><<<grid, STPB, RingI::kBytes, s>>>(B);
-    else k2_classify<false, false><<<grid, STPB, Ring::kBytes, s>>>(B);
+    if (ids) launch_pdl(k2_classify<false, true>, grid, STPB, RingI::kBytes, s, B);
+    else launch_pdl(k2_classify<false, false>, grid, STPB, Ring::kBytes, s, B);
   }
 }
 

@@ -170,6 +170,8 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
   __shared__ uint32_t s_ws[SWARPS + 1];
   __shared__ int s_last;
   Ctl* c = B.ctl;
+  pdl_wait();               // K2's classes and farthest records are complete and visible
+  pdl_launch_dependents();  // the round kernel may be scheduled on SMs this kernel frees
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n = B.n;
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
 
   // ---- table phase (S = 2: the lower chain P0->Pr and the upper chain Pr->P0) ----
   if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) c->mark[3] = globaltimer_ns() - c->t0_ns;
     R.init();
     uint32_t ns = 0, Slon = 1;
     for (int s = 0; s < 2; ++s) {
@@ -312,6 +315,7 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
   c->m_cur = mn;
   c->nruns = gridDim.x;
   if (mn == 0) c->status = ST_DONE;
+  c->mark[4] = globaltimer_ns() - c->t0_ns;
   __threadfence();
 }
 
@@ -494,6 +498,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   __shared__ uint32_t s_off;
   __shared__ uint32_t s_pref[MAX_RUNS + 1];
   Ctl* c = B.ctl;
+  pdl_wait();  // round 1 (K3) is complete and visible
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   uint32_t r = *(volatile uint32_t*)&c->round + 1;
   uint32_t S = *(volatile uint32_t*)&c->S_cur;
@@ -505,6 +510,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   uint32_t P = gridDim.x;
   bool recs_smem = false;  // this round's input records live in this CTA's smem
   uint32_t kbase = 0;      // live tiles this CTA consumed in earlier rounds
+  if (blockIdx.x == 0 && threadIdx.x == 0) c->mark[5] = globaltimer_ns() - c->t0_ns;
   unsigned long long t_table = 0, t_points = 0;  // CTA 0 phase timestamps
   if (threadIdx.x == 0) {
     for (int i = 0; i < LIVE_NS; ++i) {
@@ -751,6 +757,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
         c->m_cur = m;
         c->nruns = nruns;
         c->status = mn == 0 ? ST_DONE : ST_INTERNAL;  // hull.cpp:265-267
+        c->mark[6] = globaltimer_ns() - c->t0_ns;
         __threadfence();
       }
       return;
@@ -801,18 +808,38 @@ cudaError_t configure_stream_kernels_k3() {
                               (int)K3Layout<true>::kBytes);
 }
 
+template <class K>
+static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaStream_t s,
+                              const Bufs& B, bool cooperative) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  if (cooperative) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kernel, B);
+}
+
 void launch_k3(const Bufs& B, bool ids, int grid, cudaStream_t s) {
   if (ids)
-    k3_round1<true><<<grid, STPB, K3Layout<true>::kBytes, s>>>(B);
+    launch_pdl(k3_round1<true>, grid, STPB, K3Layout<true>::kBytes, s, B, false);
   else
-    k3_round1<false><<<grid, STPB, K3Layout<false>::kBytes, s>>>(B);
+    launch_pdl(k3_round1<false>, grid, STPB, K3Layout<false>::kBytes, s, B, false);
 }
 
 cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s) {
-  Bufs b = B;
-  void* args[] = {&b};
-  return cudaLaunchCooperativeKernel((const void*)k_rounds, dim3(grid), dim3(RTPB), args,
-                                     sizeof(RoundSmem), s);
+  return launch_pdl(k_rounds, grid, RTPB, sizeof(RoundSmem), s, B, true);
 }
 
 void launch_k5(const Bufs& B, double* ox, double* oy, long long* oidx, uint64_t cap,

@@ -315,12 +315,11 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   const uint64_t ntiles = (n + STREAM_T - 1) / STREAM_T;
   const int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ws.stream_grid));
   B.run_q = (uint32_t)((ntiles + gs - 1) / gs * STREAM_T);
+  // K1 -> K2 -> K3 -> rounds with programmatic dependent launch: no events
+  // between them (per-kernel times come from device %globaltimer marks)
   launch_k1(B, ids, gs, st);
-  if (timings) CK(cudaEventRecord(ws.ev[2], st));
   launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, ids, gs, st);
-  if (timings) CK(cudaEventRecord(ws.ev[3], st));
   launch_k3(B, ids, gs, st);
-  if (timings) CK(cudaEventRecord(ws.ev[4], st));
   CK(cudaGetLastError());
   // the round kernel's CTA j owns run j of each live set: at most gs runs
   CK(launch_rounds(B, std::min(ws.rounds_grid, gs), st));
@@ -502,15 +501,19 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
         CK(cudaEventElapsedTime(&v, ws->ev[i], ws->ev[j]));
         return (double)v;
       };
+      // kernel times from the device marks (ns since K1 started); each span
+      // runs from the previous kernel's end, so launch gaps are included
+      const unsigned long long* mk = c.mark;
+      const double k1 = mk[0] * 1e-6, k2 = mk[2] * 1e-6, k3 = mk[4] * 1e-6, kr = mk[6] * 1e-6;
       res->kernels.h2d_ms = el(0, 1);
-      res->kernels.extremes_ms = el(1, 2);
-      res->kernels.filter_ms = el(2, 3);
-      res->kernels.first_round_ms = el(3, 4);
-      res->kernels.rounds_ms = el(4, 5);
+      res->kernels.extremes_ms = k1;
+      res->kernels.filter_ms = k2 > k1 ? k2 - k1 : 0.0;
+      res->kernels.first_round_ms = k3 > k2 ? k3 - k2 : 0.0;
+      res->kernels.rounds_ms = kr > k3 ? kr - k3 : 0.0;
       res->kernels.d2h_ms = el(5, 6);
-      res->phases.pre_ms = el(1, 3);
-      res->phases.split_ms = el(3, 4);
-      res->phases.recurse_ms = el(4, 5);
+      res->phases.pre_ms = k2;
+      res->phases.split_ms = res->kernels.first_round_ms;
+      res->phases.recurse_ms = res->kernels.rounds_ms;
       res->phases.total_ms = el(0, 6);
     }
     release(std::move(ws));

@@ -37,7 +37,10 @@ for _ in range(reps):
         buf = (ctypes.c_ulonglong * 32)()
         k = L.sh_b200_debug_last_timeline(buf, 32)
         ts = [buf[i] / 1e3 for i in range(k)]
-        print(f"   trace round {trace} (us since K1 start; tile wait begin/end):", [round(t, 2) for t in ts])
+        if trace == 255:
+            print("   kernel marks (us): K1 start 0, K1 end %.1f | K2 start %.1f end %.1f | K3 start %.1f end %.1f | KR start %.1f" % tuple(ts[1:7]))
+        else:
+            print(f"   trace round {trace} (us since K1 start; tile wait begin/end):", [round(t, 2) for t in ts])
         cb = (ctypes.c_ulonglong * 1024)()
         L.sh_b200_debug_last_ctas(cb, 1024)
         ends = sorted(cb[i] / 1e3 for i in range(1024) if cb[i])
