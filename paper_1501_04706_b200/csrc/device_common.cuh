@@ -391,7 +391,7 @@ SH_DEV void mbar_wait(unsigned long long* bar, uint32_t parity) {
 // T % 64 == 0; the global arrays must be 16-byte aligned (the host stages
 // unaligned inputs).  A tile's last (cnt % 4) points are not copied (bulk
 // copies move multiples of 16 bytes); consumers read those from global.
-template <int T, int NS, bool IDS, int AUX = 0>
+template <int T, int NS, bool IDS, int AUX = 0, int NCW = 15>
 struct TileRing {
   // AUX: bytes per 64-point chunk of an optional side stream (K3: the chain bits)
   static constexpr size_t kAuxBytes = (size_t)(T / 64) * AUX;
@@ -415,7 +415,7 @@ struct TileRing {
   SH_DEV void init() {  // thread 0, followed by __syncthreads by the caller
     for (int s = 0; s < NS; ++s) {
       mbar_init(bar + s, 1);
-      mbar_init(ebar + s, CWARPS);
+      mbar_init(ebar + s, NCW);
     }
     mbar_fence_init();
   }
@@ -452,13 +452,13 @@ namespace shb {
 
 // Streams this CTA's share of the input through the ring: tiles b, b+G, ...
 // (mapped to ntiles-1-t when `reverse`), calling body(stage, first, cnt) in
-// the CWARPS consumer warps for each tile after its bytes landed.  Warp
-// CWARPS is a dedicated producer: it refills a stage as soon as every
+// the NCW consumer warps for each tile after its bytes landed.  Warp
+// NCW is a dedicated producer: it refills a stage as soon as every
 // consumer warp released it (empty mbarrier), so no consumer ever waits for
 // another consumer and no CTA-wide barrier is needed per tile.  The caller
 // initialised the ring (+ __syncthreads); a __syncthreads ends the stream.
-template <int T, int NS, bool IDS, int AUX, class Body>
-SH_DEV void stream_input(TileRing<T, NS, IDS, AUX>& R, uint32_t n, const double* X,
+template <int T, int NS, bool IDS, int AUX, int NCW, class Body>
+SH_DEV void stream_input(TileRing<T, NS, IDS, AUX, NCW>& R, uint32_t n, const double* X,
                          const double* Y, const uint32_t* I, const unsigned char* A, bool reverse,
                          const Body& body) {
   const uint32_t ntiles = (n + T - 1) / T;
@@ -468,7 +468,7 @@ SH_DEV void stream_input(TileRing<T, NS, IDS, AUX>& R, uint32_t n, const double*
     const uint32_t t = b + k * G;
     return reverse ? ntiles - 1 - t : t;
   };
-  if ((int)(threadIdx.x >> 5) == CWARPS) {  // producer warp
+  if ((int)(threadIdx.x >> 5) == NCW) {  // producer warp
     if ((threadIdx.x & 31) == 0) {
       for (uint32_t k = 0; k < mine; ++k) {
         const int s = (int)(k % NS);

@@ -36,18 +36,48 @@ namespace shb {
 constexpr int TPB = 256;             // K1 / K2 / K3 (streaming kernels)
 constexpr int WARPS = TPB / 32;
 constexpr int RTPB = 512;            // persistent round kernel
-constexpr int STPB = 512;            // TMA-fed streaming kernels K1/K2/K3 (one CTA per SM)
-constexpr int SWARPS = STPB / 32;
-constexpr int CWARPS = SWARPS - 1;   // consumer warps; warp CWARPS is the TMA producer
-constexpr int CTHREADS = 32 * CWARPS;
-#ifndef SHB_STREAM_T
-#define SHB_STREAM_T 1920
+// TMA-fed streaming kernels K1/K2/K3: one CTA per SM, warp CW is the TMA
+// producer, warps 0..CW-1 consume CH 64-point chunks each per tile.
+template <int TPB_, int CH_, int NS_>
+struct StreamCfg {
+  static constexpr int TPB = TPB_;
+  static constexpr int WARPS = TPB / 32;
+  static constexpr int CW = WARPS - 1;     // consumer warps
+  static constexpr int CT = 32 * CW;       // consumer threads
+  static constexpr int CH = CH_;           // chunks per consumer warp per tile
+  static constexpr int T = 64 * CW * CH;   // points per tile
+  static constexpr int NS = NS_;           // ring stages
+};
+#ifndef SHB_K1_TPB
+#define SHB_K1_TPB 512
 #endif
-#ifndef SHB_STREAM_NS
-#define SHB_STREAM_NS 4
+#ifndef SHB_K1_CH
+#define SHB_K1_CH 2
 #endif
-constexpr int STREAM_T = SHB_STREAM_T;    // points per TMA tile
-constexpr int STREAM_NS = SHB_STREAM_NS;  // ring stages (NS-1 tiles in flight while one is consumed)
+#ifndef SHB_K1_NS
+#define SHB_K1_NS 4
+#endif
+#ifndef SHB_K2_TPB
+#define SHB_K2_TPB 512
+#endif
+#ifndef SHB_K2_CH
+#define SHB_K2_CH 2
+#endif
+#ifndef SHB_K2_NS
+#define SHB_K2_NS 4
+#endif
+#ifndef SHB_K3_TPB
+#define SHB_K3_TPB 1024
+#endif
+#ifndef SHB_K3_CH
+#define SHB_K3_CH 1
+#endif
+#ifndef SHB_K3_NS
+#define SHB_K3_NS 4
+#endif
+using Cfg1 = StreamCfg<SHB_K1_TPB, SHB_K1_CH, SHB_K1_NS>;  // K1 extremes: memory-bound, light consumer
+using Cfg2 = StreamCfg<SHB_K2_TPB, SHB_K2_CH, SHB_K2_NS>;  // K2 filter: FP64-heavy consumer
+using Cfg3 = StreamCfg<SHB_K3_TPB, SHB_K3_CH, SHB_K3_NS>;  // K3 round 1: <= 64 registers at 1024 threads
 constexpr int SMALL_S = 512;         // tables up to this size are rebuilt per CTA in smem
 constexpr int NSLOT = 2 * SMALL_S;   // next-round segments of a small table
 constexpr uint32_t TAIL_M = 4096;    // live sets up to this size finish in one CTA
@@ -56,8 +86,11 @@ constexpr int STATS_EAGER = 64;      // stats read back together with the contro
 constexpr int MAX_ROUND_BLOCKS = 1024;
 constexpr int MAX_RUNS = MAX_ROUND_BLOCKS;
 constexpr int CLIST = 128;           // phase-B contender list entries per tile
-constexpr int LIVE_T = 2 * CTHREADS;  // live points per TMA tile of the round kernel (960)
+constexpr int RCWARPS = RTPB / 32 - 1;  // round kernel: consumer warps (+ 1 producer warp)
+constexpr int RCTHREADS = 32 * RCWARPS;
+constexpr int LIVE_T = 2 * RCTHREADS;  // live points per TMA tile of the round kernel (960)
 constexpr int LIVE_NS = 6;           // its ring stages
+constexpr int MAXW = 32;             // warps per CTA upper bound (shared scratch arrays)
 
 enum Status : uint32_t {
   ST_RUNNING = 0,

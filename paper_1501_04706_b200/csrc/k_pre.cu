@@ -91,8 +91,9 @@ SH_DEV void warp_reduce_ext(ExtRec* e, unsigned long long& bad) {
 
 // reduce (e, bad) over the block; result valid in thread 0
 SH_DEV void block_reduce_ext(ExtRec* e, unsigned long long& bad) {
-  __shared__ ExtRec s_e[4][SWARPS];
-  __shared__ unsigned long long s_bad[SWARPS];
+  __shared__ ExtRec s_e[4][MAXW];
+  __shared__ unsigned long long s_bad[MAXW];
+  const int nw = blockDim.x >> 5;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   warp_reduce_ext(e, bad);
   if (lane == 0) {
@@ -102,13 +103,13 @@ SH_DEV void block_reduce_ext(ExtRec* e, unsigned long long& bad) {
   __syncthreads();
   if (warp == 0) {
     for (int k = 0; k < 4; ++k) {
-      if (lane < SWARPS) {
+      if (lane < nw) {
         e[k] = s_e[k][lane];
       } else {
         e[k].pos = NONE;
       }
     }
-    bad = lane < SWARPS ? s_bad[lane] : ~0ull;
+    bad = lane < nw ? s_bad[lane] : ~0ull;
     warp_reduce_ext(e, bad);
   }
   __syncthreads();
@@ -138,13 +139,13 @@ SH_DEV void ext_visit(ExtRec (&e)[4], unsigned long long& bad, double x, double 
   }
 }
 
-using Ring = TileRing<STREAM_T, STREAM_NS, false>;
-using RingI = TileRing<STREAM_T, STREAM_NS, true>;
+template <bool IDS>
+using Ring1 = TileRing<Cfg1::T, Cfg1::NS, IDS, 0, Cfg1::CW>;
 
 template <bool IDS>
-__global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
+__global__ void __launch_bounds__(Cfg1::TPB, 1) k1_extremes(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  TileRing<STREAM_T, STREAM_NS, IDS> R;
+  Ring1<IDS> R;
   R.carve(smem_raw);
   Ctl* c = B.ctl;
   const uint32_t n = B.n;
@@ -177,18 +178,18 @@ __global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
   // forward over the input; within a thread indices only grow, so strict
   // comparisons keep the lowest index among exact duplicates
   stream_input(R, n, X, Y, I, nullptr, false, [&](int s, uint32_t first, uint32_t cnt) {
-    const double* xs = R.xs + s * STREAM_T;
-    const double* ys = R.ys + s * STREAM_T;
-    const uint32_t* is = R.is + s * STREAM_T;
+    const double* xs = R.xs + s * Cfg1::T;
+    const double* ys = R.ys + s * Cfg1::T;
+    const uint32_t* is = R.is + s * Cfg1::T;
     const double t0 = okey_dec(*(volatile unsigned long long*)&s_thr[0]);
     const double t1 = okey_dec(*(volatile unsigned long long*)&s_thr[1]);
     const double t2 = okey_dec(*(volatile unsigned long long*)&s_thr[2]);
     const double t3 = okey_dec(*(volatile unsigned long long*)&s_thr[3]);
     bool moved = false;
-    if (cnt == (uint32_t)STREAM_T) {
+    if (cnt == (uint32_t)Cfg1::T) {
 #pragma unroll
-      for (int k = 0; k < STREAM_T / 2 / CTHREADS; ++k) {
-        const uint32_t p = k * CTHREADS + threadIdx.x;
+      for (int k = 0; k < Cfg1::T / 2 / Cfg1::CT; ++k) {
+        const uint32_t p = k * Cfg1::CT + threadIdx.x;
         const double2 xv = reinterpret_cast<const double2*>(xs)[p];
         const double2 yv = reinterpret_cast<const double2*>(ys)[p];
         // can either point reach an extreme, or is it non-finite (exponent
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
       }
     } else {
       const uint32_t c4 = cnt & ~3u;
-      for (uint32_t j = threadIdx.x; j < cnt; j += CTHREADS) {
+      for (uint32_t j = threadIdx.x; j < cnt; j += Cfg1::CT) {
         const uint32_t i = first + j;
         const bool sm = j < c4;
         const double x = sm ? xs[j] : __ldg(X + i);
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(STPB, 1) k1_extremes(Bufs B) {
   // last CTA: combine the per-CTA partials
   for (int k = 0; k < 4; ++k) e[k].pos = NONE;
   bad = ~0ull;
-  for (uint32_t p = threadIdx.x; p < gridDim.x; p += STPB) {
+  for (uint32_t p = threadIdx.x; p < gridDim.x; p += blockDim.x) {
     const K1Partial* qp = B.k1part + p;
     ExtRec o[4];
     for (int k = 0; k < 4; ++k) {
@@ -325,9 +326,9 @@ SH_DEV void cand_visit(Cand& a, double d, double x, double y, uint32_t id, uint3
 }
 
 template <bool FILTER, bool IDS>
-__global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
+__global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  TileRing<STREAM_T, STREAM_NS, IDS> R;
+  TileRing<Cfg2::T, Cfg2::NS, IDS, 0, Cfg2::CW> R;
   R.carve(smem_raw);
   Ctl* c = B.ctl;
   pdl_wait();               // K1's extremes are complete and visible
@@ -378,12 +379,15 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
   };
 
   // backwards over the input: K1 just left the tail in L2, K3 starts at the head
-  constexpr int NCH = STREAM_T / 64 / CWARPS;  // chunks per consumer warp per tile
+  constexpr int NCH = Cfg2::T / 64 / Cfg2::CW;  // chunks per consumer warp per tile
   constexpr int NP = 2 * NCH;                  // points per thread per tile
-  stream_input(R, n, X, Y, I, nullptr, true, [&](int s, uint32_t first, uint32_t cnt) {
-    const double* xs = R.xs + s * STREAM_T;
-    const double* ys = R.ys + s * STREAM_T;
-    const uint32_t* is = R.is + s * STREAM_T;
+#ifndef SHB_K2_REVERSE
+#define SHB_K2_REVERSE 1
+#endif
+  stream_input(R, n, X, Y, I, nullptr, SHB_K2_REVERSE != 0, [&](int s, uint32_t first, uint32_t cnt) {
+    const double* xs = R.xs + s * Cfg2::T;
+    const double* ys = R.ys + s * Cfg2::T;
+    const uint32_t* is = R.is + s * Cfg2::T;
     const uint32_t c4 = cnt & ~3u;
     double px[NP], py[NP];
     uint32_t pid[NP];
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
     // ---- gather the thread's points (pairs of one 64-point chunk) ----
 #pragma unroll
     for (int kk = 0; kk < NCH; ++kk) {
-      const uint32_t cc = kk * CWARPS + warp;  // chunk of 64 points within the tile
+      const uint32_t cc = kk * Cfg2::CW + warp;  // chunk of 64 points within the tile
       const uint32_t j = cc * 64 + 2 * lane;   // this lane's pair
       double2 xv = make_double2(0.0, 0.0), yv = xv;
       uint2 iv = make_uint2(0u, 0u);
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
     const double ad0 = a0.d, ad1 = a1.d;
 #pragma unroll
     for (int kk = 0; kk < NCH; ++kk) {
-      const uint32_t cc = kk * CWARPS + warp;
+      const uint32_t cc = kk * Cfg2::CW + warp;
       if (cc * 64 >= cnt) break;  // warp-uniform
       uint32_t lw2 = 0, up2 = 0;
 #pragma unroll
@@ -481,8 +485,9 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
   });
 
   // block reduction of the two chains' farthest candidates
-  __shared__ Cand s_a[2][SWARPS];
-  __shared__ uint32_t s_kept[SWARPS];
+  __shared__ Cand s_a[2][MAXW];
+  __shared__ uint32_t s_kept[MAXW];
+  const int nwb = blockDim.x >> 5;
   __shared__ int s_last;
   a0 = warp_best(a0, true);
   a1 = warp_best(a1, false);
@@ -496,14 +501,14 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
   }
   __syncthreads();
   if (warp == 0) {
-    a0 = lane < SWARPS ? s_a[0][lane] : empty_cand();
-    a1 = lane < SWARPS ? s_a[1][lane] : empty_cand();
+    a0 = lane < nwb ? s_a[0][lane] : empty_cand();
+    a1 = lane < nwb ? s_a[1][lane] : empty_cand();
     a0 = warp_best(a0, true);
     a1 = warp_best(a1, false);
     if (lane == 0) {
       unsigned long long kb = 0;
       bool nc = false;
-      for (int w = 0; w < SWARPS; ++w) {
+      for (int w = 0; w < nwb; ++w) {
         kb += s_kept[w] & 0x7FFFFFFFu;
         nc = nc || (s_kept[w] >> 31);
       }
@@ -546,26 +551,27 @@ __global__ void __launch_bounds__(STPB, 1) k2_classify(Bufs B) {
 // host-side launch wrappers
 // ===========================================================================
 
-size_t stream_smem_bytes(bool ids) { return ids ? RingI::kBytes : Ring::kBytes; }
+template <bool IDS>
+using Ring2 = TileRing<Cfg2::T, Cfg2::NS, IDS, 0, Cfg2::CW>;
 
 cudaError_t configure_stream_kernels_pre() {
   cudaError_t e;
-  e = cudaFuncSetAttribute(k1_extremes<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring::kBytes);
+  e = cudaFuncSetAttribute(k1_extremes<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring1<false>::kBytes);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k1_extremes<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RingI::kBytes);
+  e = cudaFuncSetAttribute(k1_extremes<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring1<true>::kBytes);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k2_classify<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring::kBytes);
+  e = cudaFuncSetAttribute(k2_classify<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring2<false>::kBytes);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k2_classify<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring::kBytes);
+  e = cudaFuncSetAttribute(k2_classify<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring2<false>::kBytes);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k2_classify<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RingI::kBytes);
+  e = cudaFuncSetAttribute(k2_classify<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring2<true>::kBytes);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k2_classify<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RingI::kBytes);
+  return cudaFuncSetAttribute(k2_classify<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring2<true>::kBytes);
 }
 
 void launch_k1(const Bufs& B, bool ids, int grid, cudaStream_t s) {
-  if (ids) k1_extremes<true><<<grid, STPB, RingI::kBytes, s>>>(B);
-  else k1_extremes<false><<<grid, STPB, Ring::kBytes, s>>>(B);
+  if (ids) k1_extremes<true><<<grid, Cfg1::TPB, Ring1<true>::kBytes, s>>>(B);
+  else k1_extremes<false><<<grid, Cfg1::TPB, Ring1<false>::kBytes, s>>>(B);
 }
 
 // launch with programmatic stream serialization (PDL): the kernel's own
@@ -595,11 +601,11 @@ static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaSt
 
 void launch_k2(const Bufs& B, bool filter, bool ids, int grid, cudaStream_t s) {
   if (filter) {
-    if (ids) launch_pdl(k2_classify<true, true>, grid, STPB, RingI::kBytes, s, B);
-    else launch_pdl(k2_classify<true, false>, grid, STPB, Ring::kBytes, s, B);
+    if (ids) launch_pdl(k2_classify<true, true>, grid, Cfg2::TPB, Ring2<true>::kBytes, s, B);
+    else launch_pdl(k2_classify<true, false>, grid, Cfg2::TPB, Ring2<false>::kBytes, s, B);
   } else {
-    if (ids) launch_pdl(k2_classify<false, true>, grid, STPB, RingI::kBytes, s, B);
-    else launch_pdl(k2_classify<false, false>, grid, STPB, Ring::kBytes, s, B);
+    if (ids) launch_pdl(k2_classify<false, true>, grid, Cfg2::TPB, Ring2<true>::kBytes, s, B);
+    else launch_pdl(k2_classify<false, false>, grid, Cfg2::TPB, Ring2<false>::kBytes, s, B);
   }
 }
 

@@ -147,18 +147,17 @@ SH_DEV uint32_t sum_runs(const uint32_t* cnt, uint32_t nruns, uint32_t* s_ws) {
 // K3: round 1 straight from the input
 // ===========================================================================
 
-constexpr int K3_NS = STREAM_NS;
-constexpr int K3_NP = 2 * (STREAM_T / 64 / CWARPS);   // points per consumer thread per tile
+constexpr int K3_NP = 2 * Cfg3::CH;   // points per consumer thread per tile
 
 template <bool IDS>
 struct K3Layout {
-  using Ring = TileRing<STREAM_T, K3_NS, IDS, 16>;
+  using Ring = TileRing<Cfg3::T, Cfg3::NS, IDS, 16, Cfg3::CW>;
   static constexpr size_t kRing = (Ring::kBytes + 127) / 128 * 128;
   static constexpr size_t kBytes = kRing;
 };
 
 template <bool IDS>
-__global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
+__global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   using L = K3Layout<IDS>;
   typename L::Ring R;
@@ -167,7 +166,7 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
   __shared__ unsigned long long s_db[4];
   __shared__ SlotRec s_rec[4];
   __shared__ uint32_t s_off, s_Sn, s_Slon;
-  __shared__ uint32_t s_ws[SWARPS + 1];
+  __shared__ uint32_t s_ws[MAXW + 1];
   __shared__ int s_last;
   Ctl* c = B.ctl;
   pdl_wait();               // K2's classes and farthest records are complete and visible
@@ -229,9 +228,9 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
   // ---- point phase: forward over the input (K2 left the head in L2) ----
   stream_input(R, n, X, Y, I, reinterpret_cast<const unsigned char*>(B.bits), false,
                [&](int s, uint32_t first, uint32_t cnt) {
-    const double* xs = R.xs + s * STREAM_T;
-    const double* ys = R.ys + s * STREAM_T;
-    const uint32_t* is = R.is + s * STREAM_T;
+    const double* xs = R.xs + s * Cfg3::T;
+    const double* ys = R.ys + s * Cfg3::T;
+    const uint32_t* is = R.is + s * Cfg3::T;
     const uint4* bs = reinterpret_cast<const uint4*>(R.aux + s * L::Ring::kAuxBytes);
     const uint32_t c4 = cnt & ~3u;
     double px[K3_NP], py[K3_NP], pd[K3_NP];
@@ -239,7 +238,7 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
     uint32_t keepm = 0, lowm = 0;
 #pragma unroll
     for (int kk = 0; kk < K3_NP / 2; ++kk) {
-      const uint32_t cc = kk * CWARPS + warp;  // chunk of 64 points within the tile
+      const uint32_t cc = kk * Cfg3::CW + warp;  // chunk of 64 points within the tile
       const uint32_t j = cc * 64 + 2 * lane;
       uint4 bits = make_uint4(0u, 0u, 0u, 0u);
       double2 xv = make_double2(0.0, 0.0), yv = xv;
@@ -324,7 +323,7 @@ __global__ void __launch_bounds__(STPB, 1) k3_round1(Bufs B) {
 // ===========================================================================
 
 constexpr int RW = RTPB / 32;          // warps per CTA
-constexpr int KR_U = LIVE_T / CTHREADS;  // live points per consumer thread per tile
+constexpr int KR_U = LIVE_T / RCTHREADS;  // live points per consumer thread per tile
 
 struct RoundSmem {
   double2 lxy[LIVE_NS][LIVE_T];    // TMA ring of live points: xy          64 KB
@@ -515,7 +514,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < LIVE_NS; ++i) {
       mbar_init(&sm.lbar[i], 1);
-      mbar_init(&sm.lebar[i], CWARPS);
+      mbar_init(&sm.lebar[i], RCWARPS);
     }
     mbar_fence_init();
   }
@@ -604,7 +603,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       }
     };
     const int wid = threadIdx.x >> 5;
-    if (wid == CWARPS) {  // producer warp
+    if (wid == RCWARPS) {  // producer warp
       if (use_tma && (threadIdx.x & 31) == 0) {
         for (uint32_t kk = 0; kk < ntl; ++kk) {
           const uint32_t g = kbase + kk;
@@ -624,7 +623,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
           mbar_wait(&sm.lbar[st], ph);
 #pragma unroll
           for (int u = 0; u < KR_U; ++u) {
-            const uint32_t e = u * CTHREADS + threadIdx.x;
+            const uint32_t e = u * RCTHREADS + threadIdx.x;
             px[u] = py[u] = 0.0;
             pid[u] = 0;
             oseg[u] = NONE;
@@ -651,7 +650,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
           }
 #pragma unroll
           for (int u = 0; u < KR_U; ++u) {
-            const uint32_t e = u * CTHREADS + threadIdx.x;
+            const uint32_t e = u * RCTHREADS + threadIdx.x;
             px[u] = py[u] = 0.0;
             pid[u] = 0;
             oseg[u] = NONE;
@@ -833,9 +832,9 @@ static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaSt
 
 void launch_k3(const Bufs& B, bool ids, int grid, cudaStream_t s) {
   if (ids)
-    launch_pdl(k3_round1<true>, grid, STPB, K3Layout<true>::kBytes, s, B, false);
+    launch_pdl(k3_round1<true>, grid, Cfg3::TPB, K3Layout<true>::kBytes, s, B, false);
   else
-    launch_pdl(k3_round1<false>, grid, STPB, K3Layout<false>::kBytes, s, B, false);
+    launch_pdl(k3_round1<false>, grid, Cfg3::TPB, K3Layout<false>::kBytes, s, B, false);
 }
 
 cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s) {

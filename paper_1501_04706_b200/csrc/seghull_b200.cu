@@ -157,7 +157,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   size_t o_lxy[2], o_lis[2], o_rc[2], o_tx[2], o_ty[2], o_tid[2], o_sd[3], o_sw[3];
   // live set runs: K3's CTA j owns [j*run_q, (j+1)*run_q); the rounding of
   // run_q to whole tiles costs at most one tile per CTA
-  const uint64_t LN = N + 2ull * (uint64_t)di.sm_count * STREAM_T;
+  const uint64_t LN = N + 2ull * (uint64_t)di.sm_count * Cfg3::T;
   for (int p = 0; p < 2; ++p) {
     o_lxy[p] = take(16 * LN);
     o_lis[p] = take(8 * LN);
@@ -312,13 +312,18 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
     CK(cudaStreamSynchronize(st));
   }
 
-  const uint64_t ntiles = (n + STREAM_T - 1) / STREAM_T;
-  const int gs = (int)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)ws.stream_grid));
-  B.run_q = (uint32_t)((ntiles + gs - 1) / gs * STREAM_T);
+  // per-kernel grids: one CTA per SM, at most one per tile
+  auto grid_of = [&](int T) {
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + T - 1) / T, (uint64_t)ws.stream_grid));
+  };
+  const int g1 = grid_of(Cfg1::T), g2 = grid_of(Cfg2::T), gs = grid_of(Cfg3::T);
+  // K3's CTA j owns run j of the live set: its tiles j, j + gs, ...
+  const uint64_t ntiles3 = (n + Cfg3::T - 1) / Cfg3::T;
+  B.run_q = (uint32_t)((ntiles3 + gs - 1) / gs * Cfg3::T);
   // K1 -> K2 -> K3 -> rounds with programmatic dependent launch: no events
   // between them (per-kernel times come from device %globaltimer marks)
-  launch_k1(B, ids, gs, st);
-  launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, ids, gs, st);
+  launch_k1(B, ids, g1, st);
+  launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, ids, g2, st);
   launch_k3(B, ids, gs, st);
   CK(cudaGetLastError());
   // the round kernel's CTA j owns run j of each live set: at most gs runs
