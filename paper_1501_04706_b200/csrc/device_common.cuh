@@ -165,12 +165,32 @@ SH_DEV uint32_t lanemask_lt() {
 // consistent __threadfence, which also invalidates L1).
 SH_DEV void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
+SH_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// lock word: acquire-CAS to take it, release-store to drop it (no full
+// fences: the critical section only touches the record itself)
+template <bool SHARED>
+SH_DEV bool lock_try(uint32_t* l) {
+  uint32_t old;
+  if (SHARED)
+    asm volatile("atom.acquire.cta.shared::cta.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "r"(smem_u32(l)) : "memory");
+  else
+    asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], 0, 1;" : "=r"(old) : "l"(l) : "memory");
+  return old == 0u;
+}
+template <bool SHARED>
+SH_DEV void lock_release(uint32_t* l) {
+  if (SHARED)
+    asm volatile("st.release.cta.shared::cta.u32 [%0], 0;" ::"r"(smem_u32(l)) : "memory");
+  else
+    asm volatile("st.release.gpu.global.u32 [%0], 0;" ::"l"(l) : "memory");
+}
+
 template <bool SHARED>
 SH_DEV void rec_update(SlotRec* rec, const Cand& c, bool lower) {
   bool done = false;
   while (!done) {
-    if (atomicCAS(&rec->lock, 0u, 1u) == 0u) {
-      if (SHARED) __threadfence_block(); else fence_acq_rel_gpu();
+    if (lock_try<SHARED>(&rec->lock)) {
       volatile SlotRec* v = rec;
       Cand o;
       o.id = v->id;
@@ -183,8 +203,7 @@ SH_DEV void rec_update(SlotRec* rec, const Cand& c, bool lower) {
         v->y = c.y;
         v->id = c.id;
       }
-      if (SHARED) __threadfence_block(); else fence_acq_rel_gpu();
-      atomicExch(&rec->lock, 0u);
+      lock_release<SHARED>(&rec->lock);
       done = true;
     }
   }
@@ -345,7 +364,6 @@ SH_DEV uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_sums, uint32_t* 
 // warps per scheduler at 25-37% occupancy).
 namespace shb {
 
-SH_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 SH_DEV void mbar_init(unsigned long long* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
