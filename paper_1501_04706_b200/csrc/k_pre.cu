@@ -16,6 +16,8 @@
 // on the head, where K3 starts).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "device_common.cuh"
 #include "hull_kernels.cuh"
 
@@ -384,7 +386,11 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
 #ifndef SHB_K2_REVERSE
 #define SHB_K2_REVERSE 1
 #endif
-  stream_input(R, n, X, Y, I, nullptr, SHB_K2_REVERSE != 0, [&](int s, uint32_t first, uint32_t cnt) {
+  // One tile; FULLT: cnt == T (no bounds checks anywhere).  All decisions are
+  // bitwise predicates; the rare candidate updates sit behind one
+  // warp-uniform branch.
+  auto tile = [&](auto fullt, int s, uint32_t first, uint32_t cnt) {
+    constexpr bool FULLT = decltype(fullt)::value;
     const double* xs = R.xs + s * Cfg2::T;
     const double* ys = R.ys + s * Cfg2::T;
     const uint32_t* is = R.is + s * Cfg2::T;
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
       const uint32_t j = cc * 64 + 2 * lane;   // this lane's pair
       double2 xv = make_double2(0.0, 0.0), yv = xv;
       uint2 iv = make_uint2(0u, 0u);
-      if (j + 1 < c4) {
+      if (FULLT || j + 1 < c4) {
         xv = reinterpret_cast<const double2*>(xs)[j >> 1];
         yv = reinterpret_cast<const double2*>(ys)[j >> 1];
         if (IDS) iv = reinterpret_cast<const uint2*>(is)[j >> 1];
@@ -418,8 +424,8 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
       py[2 * kk] = yv.x; py[2 * kk + 1] = yv.y;
       pid[2 * kk] = IDS ? iv.x : first + j;
       pid[2 * kk + 1] = IDS ? iv.y : first + j + 1;
-      pv[2 * kk] = j < cnt;
-      pv[2 * kk + 1] = j + 1 < cnt;
+      pv[2 * kk] = FULLT || j < cnt;
+      pv[2 * kk + 1] = FULLT || j + 1 < cnt;
     }
     // ---- arithmetic of all NP points in one branch-free block ----
     // (the RN operations of cross(), geometry.hpp:17-19, with the per-point
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
         inside = true;
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq)
-          if (qq < ne) inside = inside && (cross_e(Q[qq], x, y) > 0.0);
+          if (qq < ne) inside = inside & (cross_e(Q[qq], x, y) > 0.0);
       }
       ins[q] = inside;
     }
@@ -453,35 +459,49 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
     const double m0 = fmax(a0.d, __longlong_as_double(*(volatile long long*)&s_dmax[0]));
     const double m1 = fmax(a1.d, __longlong_as_double(*(volatile long long*)&s_dmax[1]));
     const double ad0 = a0.d, ad1 = a1.d;
+    uint32_t lwm = 0, upm = 0, c0m = 0, c1m = 0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const uint32_t i = first + (q >> 1) * (64 * Cfg2::CW) + warp * 64 + 2 * lane + (q & 1);
+      const bool keep = pv[q] & !ins[q];
+      noncol = noncol | (pv[q] & (cl[q] != 0.0));
+      const bool member = keep & (i != p0) & (i != pr);
+      const bool neg = cl[q] < 0.0;          // hull.cpp:115-117
+      const bool lw = member & neg, up = member & !neg;
+      kept += keep;
+      lwm |= (uint32_t)lw << q;
+      upm |= (uint32_t)up << q;
+      // a candidate only when d reaches the running maximum (dl = -cl > 0 for lw)
+      c0m |= (uint32_t)(lw & (-cl[q] >= m0)) << q;
+      c1m |= (uint32_t)(up & (du[q] > 0.0) & (du[q] >= m1)) << q;
+    }
+    if (__any_sync(FULL, c0m | c1m)) {  // rare after a CTA's first tiles
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const uint32_t i = first + (q >> 1) * (64 * Cfg2::CW) + warp * 64 + 2 * lane + (q & 1);
+        if ((c0m >> q) & 1u) cand_visit(a0, -cl[q], px[q], py[q], pid[q], i, true);
+        if ((c1m >> q) & 1u) cand_visit(a1, du[q], px[q], py[q], pid[q], i, false);
+      }
+    }
 #pragma unroll
     for (int kk = 0; kk < NCH; ++kk) {
       const uint32_t cc = kk * Cfg2::CW + warp;
-      if (cc * 64 >= cnt) break;  // warp-uniform
-      uint32_t lw2 = 0, up2 = 0;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = 2 * kk + h;
-        const uint32_t i = first + cc * 64 + 2 * lane + h;
-        const bool keep = pv[q] && !ins[q];
-        noncol = noncol || (pv[q] && cl[q] != 0.0);
-        const bool member = keep && i != p0 && i != pr;
-        const bool lw = member && cl[q] < 0.0;  // hull.cpp:115-117
-        const bool up = member && !(cl[q] < 0.0);
-        lw2 |= (uint32_t)lw << h;
-        up2 |= (uint32_t)up << h;
-        kept += keep;
-        // the candidates only move when d reaches the running maximum
-        const double dl = -cl[q];
-        if (lw && dl > 0.0 && dl >= m0) cand_visit(a0, dl, px[q], py[q], pid[q], i, true);
-        if (up && du[q] > 0.0 && du[q] >= m1) cand_visit(a1, du[q], px[q], py[q], pid[q], i, false);
-      }
-      const uint32_t le = __ballot_sync(FULL, lw2 & 1u), lodd = __ballot_sync(FULL, lw2 & 2u);
-      const uint32_t ue = __ballot_sync(FULL, up2 & 1u), uodd = __ballot_sync(FULL, up2 & 2u);
+      if (!FULLT && cc * 64 >= cnt) break;  // warp-uniform
+      const uint32_t le = __ballot_sync(FULL, (lwm >> (2 * kk)) & 1u);
+      const uint32_t lodd = __ballot_sync(FULL, (lwm >> (2 * kk + 1)) & 1u);
+      const uint32_t ue = __ballot_sync(FULL, (upm >> (2 * kk)) & 1u);
+      const uint32_t uodd = __ballot_sync(FULL, (upm >> (2 * kk + 1)) & 1u);
       if (lane == 0) B.bits[(first >> 6) + cc] = make_uint4(le, lodd, ue, uodd);
     }
     // publish improvements of this thread's candidates as CTA thresholds
     if (a0.d > ad0) atomicMax(&s_dmax[0], (unsigned long long)__double_as_longlong(a0.d));
     if (a1.d > ad1) atomicMax(&s_dmax[1], (unsigned long long)__double_as_longlong(a1.d));
+  };
+  stream_input(R, n, X, Y, I, nullptr, SHB_K2_REVERSE != 0, [&](int s, uint32_t first, uint32_t cnt) {
+    if (cnt == (uint32_t)Cfg2::T)
+      tile(std::true_type{}, s, first, cnt);
+    else
+      tile(std::false_type{}, s, first, cnt);
   });
 
   // block reduction of the two chains' farthest candidates
