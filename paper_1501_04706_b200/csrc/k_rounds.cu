@@ -20,6 +20,8 @@
 // output range with ONE atomicAdd and no scan/look-back is needed.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "device_common.cuh"
 #include "hull_kernels.cuh"
 
@@ -226,8 +228,10 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   uint2* Ois = B.Lis[1];
 
   // ---- point phase: forward over the input (K2 left the head in L2) ----
-  stream_input(R, n, X, Y, I, reinterpret_cast<const unsigned char*>(B.bits), false,
-               [&](int s, uint32_t first, uint32_t cnt) {
+  // FULLT: a full tile (no bounds checks); branch-free routing of every point
+  // (non-members are masked), one warp-uniform branch for the rare contenders.
+  auto tile = [&](auto fullt, int s, uint32_t first, uint32_t cnt) {
+    constexpr bool FULLT = decltype(fullt)::value;
     const double* xs = R.xs + s * Cfg3::T;
     const double* ys = R.ys + s * Cfg3::T;
     const uint32_t* is = R.is + s * Cfg3::T;
@@ -243,7 +247,12 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
       uint4 bits = make_uint4(0u, 0u, 0u, 0u);
       double2 xv = make_double2(0.0, 0.0), yv = xv;
       uint2 iv = make_uint2(0u, 0u);
-      if (cc * 64 < cnt) {
+      if (FULLT) {
+        bits = bs[cc];
+        xv = reinterpret_cast<const double2*>(xs)[j >> 1];
+        yv = reinterpret_cast<const double2*>(ys)[j >> 1];
+        if (IDS) iv = reinterpret_cast<const uint2*>(is)[j >> 1];
+      } else if (cc * 64 < cnt) {
         bits = bs[cc];
         if (j + 1 < c4) {
           xv = reinterpret_cast<const double2*>(xs)[j >> 1];
@@ -270,13 +279,29 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
         const uint32_t lw = ((h ? bits.y : bits.x) >> lane) & 1u;
         const uint32_t uw = ((h ? bits.w : bits.z) >> lane) & 1u;
         bool lower = false;
-        if ((lw | uw) && route_point<false>(s_rt + (lw ? 0 : 1), px[q], py[q], pid[q], pd[q], pseg[q], lower))
-          keepm |= 1u << q;
-        if (lw) lowm |= 1u << q;
+        const bool keep =
+            route_point<false>(s_rt + (lw ? 0 : 1), px[q], py[q], pid[q], pd[q], pseg[q], lower);
+        keepm |= (uint32_t)((lw | uw) & keep) << q;
+        lowm |= lw << q;
       }
     }
-    contend_tile<K3_NP>(s_db, s_rec, keepm, px, py, pd, pid, pseg, lowm);
+    // contenders: kept points reaching the CTA slot's running maximum
+    uint32_t candm = 0;
+#pragma unroll
+    for (int q = 0; q < K3_NP; ++q) {
+      const unsigned long long db = (unsigned long long)__double_as_longlong(pd[q]);
+      candm |= (uint32_t)(((keepm >> q) & 1u) &
+                          (db >= *(volatile unsigned long long*)&s_db[pseg[q] & 3u])) << q;
+    }
+    if (__any_sync(FULL, candm)) contend_tile<K3_NP>(s_db, s_rec, candm, px, py, pd, pid, pseg, lowm);
     run_append<K3_NP>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, run_base);
+  };
+  stream_input(R, n, X, Y, I, reinterpret_cast<const unsigned char*>(B.bits), false,
+               [&](int s, uint32_t first, uint32_t cnt) {
+    if (cnt == (uint32_t)Cfg3::T)
+      tile(std::true_type{}, s, first, cnt);
+    else
+      tile(std::false_type{}, s, first, cnt);
   });
 
   // ---- flush the CTA's records to the global slots of round 2's argmax ----
