@@ -90,7 +90,8 @@ constexpr int RCWARPS = RTPB / 32 - 1;  // round kernel: consumer warps (+ 1 pro
 constexpr int RCTHREADS = 32 * RCWARPS;
 constexpr int LIVE_T = 2 * RCTHREADS;  // live points per TMA tile of the round kernel (960)
 constexpr int LIVE_NS = 6;           // its ring stages
-constexpr int MAXW = 32;             // warps per CTA upper bound (shared scratch arrays)
+constexpr int MAXW = 32;
+constexpr uint32_t SMALL_N = 16384;  // inputs up to this size take the one-CTA path (k_small_pre)             // warps per CTA upper bound (shared scratch arrays)
 
 enum Status : uint32_t {
   ST_RUNNING = 0,

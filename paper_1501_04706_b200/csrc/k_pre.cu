@@ -141,6 +141,58 @@ SH_DEV void ext_visit(ExtRec (&e)[4], unsigned long long& bad, double x, double 
   }
 }
 
+// Thread 0, once the four extremes and the first bad index are known:
+// degenerate statuses (hull.cpp:222-237) and the quadrilateral (hull.cpp:58-74).
+SH_DEV void finalize_extremes(const Bufs& B, const ExtRec (&e)[4], unsigned long long bad) {
+  Ctl* c = B.ctl;
+  c->ticket = 0;
+  c->bad_index = bad;
+  // round-0 farthest slots (K2 offers into Slot[0]; hull_kernels.cuh)
+  rec_clear(&B.Sd[0][0], &B.Srec[0][0]);
+  rec_clear(&B.Sd[0][1], &B.Srec[0][1]);
+  c->mark[0] = globaltimer_ns() - c->t0_ns;
+  if (bad != ~0ull) {
+    c->status = ST_NONFINITE;
+    return;
+  }
+  for (int k = 0; k < 4; ++k) {
+    c->ext_x[k] = e[k].x;
+    c->ext_y[k] = e[k].y;
+    c->ext_id[k] = e[k].id;
+    c->ext_pos[k] = e[k].pos;
+  }
+  if (e[0].x == e[2].x && e[0].y == e[2].y) {  // hull.cpp:234-237
+    c->status = ST_SINGLE;
+    return;
+  }
+  // hull.cpp:58-74: corners [left, bottom, right, top], distinct count and
+  // the edges between consecutive non-equal corners (with wrap-around)
+  int distinct = 0;
+  for (int a = 0; a < 4; ++a) {
+    bool seen = false;
+    for (int b = 0; b < a; ++b) seen |= (e[a].x == e[b].x && e[a].y == e[b].y);
+    if (!seen) ++distinct;
+  }
+  int ne = 0;
+  for (int a = 0; a < 4; ++a) {
+    const ExtRec& p = e[a];
+    const ExtRec& qq = e[(a + 1) & 3];
+    if (!(p.x == qq.x && p.y == qq.y)) {
+      const Edge ed = make_edge(p.x, p.y, qq.x, qq.y);
+      c->edges[ne][0] = ed.ax;
+      c->edges[ne][1] = ed.ay;
+      c->edges[ne][2] = ed.ex;
+      c->edges[ne][3] = ed.ey;
+      ++ne;
+    }
+  }
+  for (int k = ne; k < 4; ++k)
+    for (int j = 0; j < 4; ++j) c->edges[k][j] = 0.0;
+  c->distinct = distinct;
+  c->nedges = ne;
+  c->mark[0] = globaltimer_ns() - c->t0_ns;
+}
+
 template <bool IDS>
 using Ring1 = TileRing<Cfg1::T, Cfg1::NS, IDS, 0, Cfg1::CW>;
 
@@ -266,52 +318,7 @@ __global__ void __launch_bounds__(Cfg1::TPB, 1) k1_extremes(Bufs B) {
   block_reduce_ext(e, bad);
   if (threadIdx.x != 0) return;
 
-  c->ticket = 0;
-  c->bad_index = bad;
-  // round-0 farthest slots (K2 offers into Slot[0]; hull_kernels.cuh)
-  rec_clear(&B.Sd[0][0], &B.Srec[0][0]);
-  rec_clear(&B.Sd[0][1], &B.Srec[0][1]);
-  c->mark[0] = globaltimer_ns() - c->t0_ns;
-  if (bad != ~0ull) {
-    c->status = ST_NONFINITE;
-    return;
-  }
-  for (int k = 0; k < 4; ++k) {
-    c->ext_x[k] = e[k].x;
-    c->ext_y[k] = e[k].y;
-    c->ext_id[k] = e[k].id;
-    c->ext_pos[k] = e[k].pos;
-  }
-  if (e[0].x == e[2].x && e[0].y == e[2].y) {  // hull.cpp:234-237
-    c->status = ST_SINGLE;
-    return;
-  }
-  // hull.cpp:58-74: corners [left, bottom, right, top], distinct count and
-  // the edges between consecutive non-equal corners (with wrap-around)
-  int distinct = 0;
-  for (int a = 0; a < 4; ++a) {
-    bool seen = false;
-    for (int b = 0; b < a; ++b) seen |= (e[a].x == e[b].x && e[a].y == e[b].y);
-    if (!seen) ++distinct;
-  }
-  int ne = 0;
-  for (int a = 0; a < 4; ++a) {
-    const ExtRec& p = e[a];
-    const ExtRec& qq = e[(a + 1) & 3];
-    if (!(p.x == qq.x && p.y == qq.y)) {
-      const Edge ed = make_edge(p.x, p.y, qq.x, qq.y);
-      c->edges[ne][0] = ed.ax;
-      c->edges[ne][1] = ed.ay;
-      c->edges[ne][2] = ed.ex;
-      c->edges[ne][3] = ed.ey;
-      ++ne;
-    }
-  }
-  for (int k = ne; k < 4; ++k)
-    for (int j = 0; j < 4; ++j) c->edges[k][j] = 0.0;
-  c->distinct = distinct;
-  c->nedges = ne;
-  c->mark[0] = globaltimer_ns() - c->t0_ns;
+  finalize_extremes(B, e, bad);
 }
 
 // ===========================================================================
@@ -568,6 +575,165 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
 }
 
 // ===========================================================================
+// KS: small inputs (n <= SMALL_N) -- K1 + K2 + the round-0 compaction in ONE
+// CTA, handing a dense live set straight to the round kernel at round 1.
+// Used for the shard-hull merge of the multi-GPU path (~50 x N points) and
+// other tiny inputs, where four launches and multi-CTA tails dominate.
+// ===========================================================================
+
+template <bool FILTER, bool IDS>
+__global__ void __launch_bounds__(1024, 1) k_small_pre(Bufs B) {
+  Ctl* c = B.ctl;
+  const uint32_t n = B.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* __restrict__ X = B.in_x;
+  const double* __restrict__ Y = B.in_y;
+  const uint32_t* __restrict__ I = B.in_id;
+  if (threadIdx.x == 0) c->t0_ns = globaltimer_ns();
+
+  // ---- extremes (hull.cpp:25-45); indices grow within a thread ----
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  ExtRec e[4];
+  e[0].x = INF;  e[0].y = INF;
+  e[1].x = -INF; e[1].y = INF;
+  e[2].x = -INF; e[2].y = -INF;
+  e[3].x = INF;  e[3].y = -INF;
+  for (int k = 0; k < 4; ++k) e[k].id = e[k].pos = NONE;
+  unsigned long long bad = ~0ull;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+    ext_visit<IDS>(e, bad, __ldg(X + i), __ldg(Y + i), IDS ? __ldg(I + i) : i, i);
+  block_reduce_ext(e, bad);
+  if (threadIdx.x == 0) finalize_extremes(B, e, bad);
+  __syncthreads();
+  if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
+
+  // ---- filter + classes + round-0 farthest + dense member list (K2) ----
+  const uint32_t p0 = c->ext_pos[0], pr = c->ext_pos[2];
+  const double x0 = c->ext_x[0], y0 = c->ext_y[0], xr = c->ext_x[2], yr = c->ext_y[2];
+  const Edge E01 = make_edge(x0, y0, xr, yr);
+  const Edge E10 = make_edge(xr, yr, x0, y0);
+  const bool filt = FILTER && c->distinct >= 3;
+  const int ne = filt ? c->nedges : 0;
+  Edge Q[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    Q[k].ax = c->edges[k][0];
+    Q[k].ay = c->edges[k][1];
+    Q[k].ex = c->edges[k][2];
+    Q[k].ey = c->edges[k][3];
+  }
+  __shared__ uint32_t s_off;
+  __shared__ Cand s_a[2][MAXW];
+  __shared__ uint32_t s_kept[MAXW];
+  if (threadIdx.x == 0) s_off = 0;
+  __syncthreads();
+  double2* Oxy = B.Lxy[0];
+  uint2* Ois = B.Lis[0];
+  Cand a0 = empty_cand(), a1 = empty_cand();
+  uint32_t kept = 0;
+  bool noncol = false;
+  for (uint32_t b0 = 0; b0 < n; b0 += blockDim.x) {
+    const uint32_t i = b0 + threadIdx.x;
+    const bool valid = i < n;
+    double x = 0.0, y = 0.0;
+    uint32_t id = 0;
+    if (valid) {
+      x = __ldg(X + i);
+      y = __ldg(Y + i);
+      id = IDS ? __ldg(I + i) : i;
+    }
+    const double cl = cross_e(E01, x, y);  // cross(P0, Pr, p)
+    bool inside = false;
+    if (filt) {  // hull.cpp:80-90
+      inside = valid;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq)
+        if (qq < ne) inside = inside && (cross_e(Q[qq], x, y) > 0.0);
+    }
+    const bool keep = valid && !inside;
+    kept += keep;
+    noncol = noncol || (valid && cl != 0.0);
+    const bool member = keep && i != p0 && i != pr;
+    const bool lw = member && cl < 0.0;  // hull.cpp:115-117
+    if (lw) cand_visit(a0, -cl, x, y, id, i, true);
+    else if (member) cand_visit(a1, outward_e(E10, x, y), x, y, id, i, false);
+    // dense append: seg 0 = lower chain, 1 = upper chain
+    const uint32_t bal = __ballot_sync(FULL, member);
+    uint32_t off = 0;
+    if (lane == 0 && bal) off = atomicAdd(&s_off, (uint32_t)__popc(bal));
+    off = __shfl_sync(FULL, off, 0);
+    if (member) {
+      const uint32_t p = off + __popc(bal & lanemask_lt());
+      Oxy[p] = make_double2(x, y);
+      Ois[p] = make_uint2(id, lw ? 0u : 1u);
+    }
+  }
+  a0 = warp_best(a0, true);
+  a1 = warp_best(a1, false);
+  const bool nc_any = __any_sync(FULL, noncol);
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) kept += __shfl_xor_sync(FULL, kept, m);
+  if (lane == 0) {
+    s_a[0][warp] = a0;
+    s_a[1][warp] = a1;
+    s_kept[warp] = kept | (nc_any ? 0x80000000u : 0u);
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  const int nwb = blockDim.x >> 5;
+  a0 = lane < nwb ? s_a[0][lane] : empty_cand();
+  a1 = lane < nwb ? s_a[1][lane] : empty_cand();
+  a0 = warp_best(a0, true);
+  a1 = warp_best(a1, false);
+  if (lane != 0) return;
+  unsigned long long kb = 0;
+  bool nc = false;
+  for (int w = 0; w < nwb; ++w) {
+    kb += s_kept[w] & 0x7FFFFFFFu;
+    nc = nc || (s_kept[w] >> 31);
+  }
+  const uint32_t m = s_off;
+  c->kept = kb;
+  // round-1 farthest records (Slot[0]) and cleared round-1 offer slots (Slot[1])
+  const Cand* ab[2] = {&a0, &a1};
+  for (int t = 0; t < 2; ++t) {
+    rec_clear(&B.Sd[0][t], &B.Srec[0][t]);
+    if (ab[t]->d > 0.0) {
+      B.Sd[0][t] = (unsigned long long)__double_as_longlong(ab[t]->d);
+      B.Srec[0][t].d = ab[t]->d;
+      B.Srec[0][t].x = ab[t]->x;
+      B.Srec[0][t].y = ab[t]->y;
+      B.Srec[0][t].id = ab[t]->id;
+    }
+  }
+  for (int t = 0; t < 4; ++t) rec_clear(&B.Sd[1][t], &B.Srec[1][t]);
+  if (!nc) {
+    c->status = ST_COLLINEAR;  // hull.cpp:238-248
+  } else {
+    B.Tx[0][0] = x0;
+    B.Ty[0][0] = y0;
+    B.Tid[0][0] = c->ext_id[0];
+    B.Tx[0][1] = xr;
+    B.Ty[0][1] = yr;
+    B.Tid[0][1] = c->ext_id[2];
+    if (m & 1u) {  // pad the run to an even length
+      Oxy[m] = make_double2(0.0, 0.0);
+      Ois[m] = make_uint2(NONE, NONE);
+    }
+    B.run_cnt[0][0] = m;
+    c->nruns = 1;
+    c->S_cur = 2;
+    c->Slo_cur = 1;
+    c->m_cur = m;
+    c->round = 0;
+    if (m == 0) c->status = ST_DONE;
+  }
+  c->mark[2] = globaltimer_ns() - c->t0_ns;
+  c->mark[4] = c->mark[2];
+  __threadfence();
+}
+
+// ===========================================================================
 // host-side launch wrappers
 // ===========================================================================
 
@@ -587,6 +753,16 @@ cudaError_t configure_stream_kernels_pre() {
   e = cudaFuncSetAttribute(k2_classify<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring2<true>::kBytes);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k2_classify<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring2<true>::kBytes);
+}
+
+void launch_small(const Bufs& B, bool filter, bool ids, cudaStream_t s) {
+  if (filter) {
+    if (ids) k_small_pre<true, true><<<1, 1024, 0, s>>>(B);
+    else k_small_pre<true, false><<<1, 1024, 0, s>>>(B);
+  } else {
+    if (ids) k_small_pre<false, true><<<1, 1024, 0, s>>>(B);
+    else k_small_pre<false, false><<<1, 1024, 0, s>>>(B);
+  }
 }
 
 void launch_k1(const Bufs& B, bool ids, int grid, cudaStream_t s) {

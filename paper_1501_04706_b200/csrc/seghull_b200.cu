@@ -22,6 +22,7 @@
 
 namespace shb {
 void launch_k1(const Bufs& B, bool ids, int grid, cudaStream_t s);
+void launch_small(const Bufs& B, bool filter, bool ids, cudaStream_t s);
 void launch_k2(const Bufs& B, bool filter, bool ids, int grid, cudaStream_t s);
 void launch_k3(const Bufs& B, bool ids, int grid, cudaStream_t s);
 cudaError_t configure_stream_kernels_pre();
@@ -312,6 +313,16 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
     CK(cudaStreamSynchronize(st));
   }
 
+  if (n <= SMALL_N) {
+    // one CTA does K1 + K2 + the round-0 compaction, the round kernel takes
+    // over at round 1 with as many CTAs as the live set can use
+    const int gr = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 1919) / 1920, ws.rounds_grid));
+    B.run_q = (uint32_t)(((n + gr - 1) / gr + 2 + 1) & ~1ull);
+    launch_small(B, rq.mode == SH_MODE_WITH_PREPROCESS, ids, st);
+    CK(cudaGetLastError());
+    CK(launch_rounds(B, gr, st));
+    out.launches = 2;
+  } else {
   // per-kernel grids: one CTA per SM, at most one per tile
   auto grid_of = [&](int T) {
     return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + T - 1) / T, (uint64_t)ws.stream_grid));
@@ -329,6 +340,7 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   // the round kernel's CTA j owns run j of each live set: at most gs runs
   CK(launch_rounds(B, std::min(ws.rounds_grid, gs), st));
   out.launches = 4;
+  }
   if (timings) CK(cudaEventRecord(ws.ev[5], st));
   const bool out_dev = (rq.flags & SH_OUT_DEVICE) != 0;
   if (out_dev && (res.x || res.y || res.idx)) {
