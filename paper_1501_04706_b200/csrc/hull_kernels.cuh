@@ -85,13 +85,12 @@ constexpr int STATS_CAP = 1 << 16;
 constexpr int STATS_EAGER = 64;      // stats read back together with the control block
 constexpr int MAX_ROUND_BLOCKS = 1024;
 constexpr int MAX_RUNS = MAX_ROUND_BLOCKS;
-constexpr int CLIST = 128;           // phase-B contender list entries per tile
 constexpr int RCWARPS = RTPB / 32 - 1;  // round kernel: consumer warps (+ 1 producer warp)
 constexpr int RCTHREADS = 32 * RCWARPS;
 constexpr int LIVE_T = 2 * RCTHREADS;  // live points per TMA tile of the round kernel (960)
 constexpr int LIVE_NS = 6;           // its ring stages
-constexpr int MAXW = 32;
-constexpr uint32_t SMALL_N = 16384;  // inputs up to this size take the one-CTA path (k_small_pre)             // warps per CTA upper bound (shared scratch arrays)
+constexpr int MAXW = 32;             // warps per CTA upper bound (shared scratch arrays)
+constexpr uint32_t SMALL_N = 16384;  // inputs up to this size take the one-CTA path (k_small_pre)
 
 enum Status : uint32_t {
   ST_RUNNING = 0,
