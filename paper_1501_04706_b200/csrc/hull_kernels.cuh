@@ -87,8 +87,14 @@ constexpr int MAX_ROUND_BLOCKS = 1024;
 constexpr int MAX_RUNS = MAX_ROUND_BLOCKS;
 constexpr int RCWARPS = RTPB / 32 - 1;  // round kernel: consumer warps (+ 1 producer warp)
 constexpr int RCTHREADS = 32 * RCWARPS;
-constexpr int LIVE_T = 2 * RCTHREADS;  // live points per TMA tile of the round kernel (960)
-constexpr int LIVE_NS = 6;           // its ring stages
+#ifndef SHB_LIVE_U
+#define SHB_LIVE_U 2
+#endif
+#ifndef SHB_LIVE_NS
+#define SHB_LIVE_NS 6
+#endif
+constexpr int LIVE_T = SHB_LIVE_U * RCTHREADS;  // live points per TMA tile of the round kernel (960)
+constexpr int LIVE_NS = SHB_LIVE_NS;            // its ring stages
 constexpr int MAXW = 32;             // warps per CTA upper bound (shared scratch arrays)
 constexpr uint32_t SMALL_N = 16384;  // inputs up to this size take the one-CTA path (k_small_pre)
 
@@ -132,6 +138,14 @@ struct __align__(16) SlotRec {
   double d, x, y;
   uint32_t id;    // NONE: no candidate (segment not splittable)
   uint32_t lock;
+};
+
+// Farthest-point contender of a large-table round: a survivor whose
+// atomicMax on its new segment's distance bits returned a value <= its own.
+struct __align__(16) LiveCand {
+  double d;
+  uint32_t pos;  // position in the live set just written
+  uint32_t seg;  // new segment
 };
 
 struct StatRec {
@@ -198,9 +212,15 @@ struct Bufs {
   double* Tx[2];
   double* Ty[2];
   uint32_t* Tid[2];
-  // farthest-point slots
+  // farthest-point slots: running maximum of the distance bits per segment
+  // (S entries); records of small tables (NSLOT entries, small rounds only)
   unsigned long long* Sd[3];
   SlotRec* Srec[3];
+  // large tables: winner slot per segment = position of its farthest point
+  // in the live set the round wrote (NONE: no kept member); Lc lists, per
+  // CTA run, the survivors that reached their segment's running maximum
+  uint32_t* Wn[3];
+  LiveCand* Lc;
   Route* route;
 };
 

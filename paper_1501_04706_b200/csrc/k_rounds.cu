@@ -46,23 +46,40 @@ SH_DEV Route ldcg_route(const Route* p) {
 //   left = lower ? lex(p) < lex(C) : lex(C) < lex(p)
 //   d    = outward_distance(left ? (A, C) : (C, B), p)   (geometry.hpp:25-27)
 //   keep iff the segment splits, p is not C itself and d > 0 (hull.cpp:199)
-// The row stores A | C | B as consecutive double2, so the edge endpoints are
-// fetched by computed offset instead of being selected in registers.
+// The row stores A | C | B | meta as consecutive 16-byte words.  In shared
+// memory the edge endpoints are fetched by computed offset; from global
+// memory the whole row is loaded at once (one L2 round trip, not two).
 template <bool GLOBAL>
 SH_DEV bool route_point(const Route* rp, double x, double y, uint32_t id, double& d,
                         uint32_t& nseg, bool& lower) {
   const double2* row = reinterpret_cast<const double2*>(rp);
-  const double2 C = GLOBAL ? __ldcg(row + 1) : row[1];
-  const uint4 meta = GLOBAL ? __ldcg(reinterpret_cast<const uint4*>(row + 3))
-                            : *reinterpret_cast<const uint4*>(row + 3);  // cid, ns, flags
+  double2 A, C, Bv;
+  uint4 meta;
+  if (GLOBAL) {  // two 256-bit L2 loads (LDG.E.ENL2.256): A|C and B|meta
+    unsigned long long m0, m1;
+    asm("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(A.x), "=d"(A.y), "=d"(C.x), "=d"(C.y) : "l"(row));
+    asm("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(Bv.x), "=d"(Bv.y), "=l"(m0), "=l"(m1) : "l"(row + 2));
+    meta = make_uint4((uint32_t)m0, (uint32_t)(m0 >> 32), (uint32_t)m1, (uint32_t)(m1 >> 32));
+  } else {
+    C = row[1];
+    meta = *reinterpret_cast<const uint4*>(row + 3);
+  }
   lower = meta.z & RT_LOWER;
   const bool xeq = x == C.x;
   const bool lt = x < C.x || (xeq && y < C.y);
   const bool eq = xeq && y == C.y;
   const bool left = lower ? lt : !(lt || eq);
-  const int o = left ? 0 : 1;
-  const double2 S = GLOBAL ? __ldcg(row + o) : row[o];
-  const double2 E = GLOBAL ? __ldcg(row + o + 1) : row[o + 1];
+  double2 S, E;
+  if (GLOBAL) {
+    S = left ? A : C;
+    E = left ? C : Bv;
+  } else {
+    const int o = left ? 0 : 1;
+    S = row[o];
+    E = row[o + 1];
+  }
   d = outward_e(make_edge(S.x, S.y, E.x, E.y), x, y);
   nseg = meta.y + (left ? 0u : 1u);
   return (meta.z & RT_SPLIT) && id != meta.x && d > 0.0;
@@ -70,10 +87,13 @@ SH_DEV bool route_point(const Route* rp, double x, double y, uint32_t id, double
 
 // Dense append of this thread's survivors to the CTA's run of the next live
 // set: one shared-memory atomicAdd per warp, no global atomics, no barrier.
+// With Oc, the survivors flagged in candm are also listed (distance,
+// position, segment) at Oc[cbase + ...] through the counter s_coff.
 template <int NP>
 SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py)[NP],
                        const uint32_t (&pid)[NP], const uint32_t (&pseg)[NP], uint32_t* s_off,
-                       double2* Oxy, uint2* Ois, uint32_t base) {
+                       double2* Oxy, uint2* Ois, uint32_t base, const double (&pd)[NP] = {},
+                       uint32_t candm = 0, uint32_t* s_coff = nullptr, LiveCand* Oc = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t bal[NP];
   uint32_t tot = 0;
@@ -87,14 +107,37 @@ SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py
   if (lane == 0) off = atomicAdd(s_off, tot);
   off = base + __shfl_sync(FULL, off, 0);
   const uint32_t lt = lanemask_lt();
+  uint32_t e[NP];
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
+    e[j] = off + __popc(bal[j] & lt);
     if ((keepm >> j) & 1u) {
-      const uint32_t e = off + __popc(bal[j] & lt);
-      Oxy[e] = make_double2(px[j], py[j]);
-      Ois[e] = make_uint2(pid[j], pseg[j]);
+      Oxy[e[j]] = make_double2(px[j], py[j]);
+      Ois[e[j]] = make_uint2(pid[j], pseg[j]);
     }
     off += __popc(bal[j]);
+  }
+  if (Oc != nullptr && __any_sync(FULL, candm)) {
+    uint32_t cb[NP], ctot = 0;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      cb[j] = __ballot_sync(FULL, (candm >> j) & 1u);
+      ctot += __popc(cb[j]);
+    }
+    uint32_t co = 0;
+    if (lane == 0) co = atomicAdd(s_coff, ctot);
+    co = base + __shfl_sync(FULL, co, 0);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      if ((candm >> j) & 1u) {
+        LiveCand lc;
+        lc.d = pd[j];
+        lc.pos = e[j];
+        lc.seg = pseg[j];
+        Oc[co + __popc(cb[j] & lt)] = lc;
+      }
+      co += __popc(cb[j]);
+    }
   }
 }
 
@@ -429,30 +472,46 @@ SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, 
   __syncthreads();
 }
 
-// Large table: a grid-wide two-step scan over the P participating CTAs, each
-// thread owning TS consecutive segments (independent loads in flight).  The
-// table also clears the global farthest slots of the segments it creates.
-// Returns false on segment-table overflow (every CTA returns consistently).
+// Large table (S > SMALL_S): a grid-wide two-step scan over the P
+// participating CTAs.  Segment s splits iff it has a farthest point: its
+// winner slot Wn[sin][s] holds C's position in the input live set -- or,
+// right after a small round (from_rec), its flushed record Srec[sin][s].
+// Each warp owns 32 x TS consecutive segments per step, lane-contiguous so
+// every load and store is coalesced.  Finished segments (no split) cost one
+// head copy; only split ones build a route row and prepare the two winner
+// slots / distance maxima of their children.  Returns false on segment-table
+// overflow (every CTA returns consistently).
 constexpr int TS = 8;
 
 SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, uint32_t pout,
-                        uint32_t sin, uint32_t sout, uint32_t P, uint32_t* s_ws, uint32_t& Sn,
-                        uint32_t& Slon) {
+                        uint32_t sin, uint32_t sout, uint32_t P, bool from_rec, uint32_t* s_ws,
+                        uint32_t& Sn, uint32_t& Slon) {
   Ctl* c = B.ctl;
-  const uint32_t per = (S + P - 1) / P;
+  constexpr uint32_t STEP = RTPB * TS;
+  // CTA ranges are whole warp chunks (32 * TS), so that the lane mapping is
+  // identical in both passes
+  const uint32_t chunks = (S + 32 * TS - 1) / (32 * TS);
+  const uint32_t per = (chunks + P - 1) / P * (32 * TS);
   const uint32_t lo = min(S, blockIdx.x * per), hi = min(S, lo + per);
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t* Win = B.Wn[sin];
   const SlotRec* recs = B.Srec[sin];
-  // T1: splittable counts of this CTA's range (total and lower chain)
+  auto split_of = [&](uint32_t s) -> uint32_t {  // C's live position / record index, or NONE
+    if (s >= hi) return NONE;
+    if (from_rec) return __ldcg(&recs[s].id) != NONE ? s : NONE;
+    return __ldcg(Win + s);
+  };
+  // T1: split counts of this CTA's range (total and lower chain)
   uint32_t cnt = 0, cnt_lo = 0;
-  for (uint32_t s0 = lo + threadIdx.x * TS; s0 < hi; s0 += RTPB * TS) {
-    uint32_t ids[TS];
+  for (uint32_t g0 = lo + wid * 32 * TS; g0 < hi; g0 += STEP) {
+    uint32_t w[TS];
 #pragma unroll
-    for (int i = 0; i < TS; ++i) ids[i] = s0 + i < hi ? __ldcg(&recs[s0 + i].id) : NONE;
+    for (int i = 0; i < TS; ++i) w[i] = split_of(g0 + i * 32 + lane);
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
-      const bool split = ids[i] != NONE;
-      cnt += split;
-      cnt_lo += split && s0 + i < Slo;
+      const uint32_t s = g0 + i * 32 + lane;
+      cnt += w[i] != NONE;
+      cnt_lo += w[i] != NONE && s < Slo;
     }
   }
   {
@@ -483,28 +542,102 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
     if (blockIdx.x == 0 && threadIdx.x == 0) c->status = ST_OVERFLOW;
     return false;
   }
+  const double* Tx = B.Tx[pin];
+  const double* Ty = B.Ty[pin];
+  const uint32_t* Tid = B.Tid[pin];
+  double* Ox = B.Tx[pout];
+  double* Oy = B.Ty[pout];
+  uint32_t* Oid = B.Tid[pout];
+  uint32_t* Wout = B.Wn[sout];
+  unsigned long long* Sdo = B.Sd[sout];
+  const uint32_t lt = lanemask_lt();
   uint32_t running = pre_all;
-  for (uint32_t g0 = lo; g0 < hi; g0 += RTPB * TS) {
-    const uint32_t s0 = g0 + threadIdx.x * TS;
-    uint32_t ids[TS];
-    uint32_t mine = 0;
+  // every step covers [lo + k*STEP, lo + (k+1)*STEP): warps in order
+  for (uint32_t b0 = lo; b0 < hi; b0 += STEP) {
+    const uint32_t g0 = b0 + wid * 32 * TS;
+    uint32_t w[TS];
+#pragma unroll
+    for (int i = 0; i < TS; ++i) w[i] = split_of(g0 + i * 32 + lane);
+    uint32_t wpre[TS], wtot = 0;
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
-      ids[i] = s0 + i < hi ? __ldcg(&recs[s0 + i].id) : NONE;
-      mine += ids[i] != NONE;
+      const uint32_t bal = __ballot_sync(FULL, w[i] != NONE);
+      wpre[i] = wtot + __popc(bal & lt);
+      wtot += __popc(bal);
     }
     uint32_t total;
-    uint32_t ns = s0 + running + block_exclusive_scan(mine, s_ws, &total);
+    const uint32_t wx = block_exclusive_scan(lane == 0 ? wtot : 0u, s_ws, &total);
+    const uint32_t wbase = running + __shfl_sync(FULL, wx, 0);
+    // all loads of the step first (independent, in flight together), then
+    // the stores
+    double ax[TS], ay[TS];
+    uint32_t aid[TS];
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
-      const uint32_t s = s0 + i;
+      const uint32_t s = min(g0 + i * 32 + lane, S - 1);
+      ax[i] = __ldcg(Tx + s);
+      ay[i] = __ldcg(Ty + s);
+      aid[i] = __ldcg(Tid + s);
+    }
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      const uint32_t s = g0 + i * 32 + lane;
       if (s < hi) {
-        const Route r = make_route(B, pin, recs + s, s, S, Slo, ns);
+        const uint32_t ns = s + wbase + wpre[i];
+        Ox[ns] = ax[i];
+        Oy[ns] = ay[i];
+        Oid[ns] = aid[i];
+        Wout[ns] = NONE;
+      }
+    }
+    // split segments: route row + head C + the children's slots (loads of
+    // the whole step first again)
+    double bx[TS], by[TS], cx[TS], cy[TS];
+    uint32_t cid[TS];
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      const uint32_t s = g0 + i * 32 + lane;
+      bx[i] = by[i] = cx[i] = cy[i] = 0.0;
+      cid[i] = NONE;
+      if (s < hi && w[i] != NONE) {
+        const uint32_t sb = s + 1 == S ? 0u : s + 1;
+        bx[i] = __ldcg(Tx + sb);
+        by[i] = __ldcg(Ty + sb);
+        if (from_rec) {
+          cx[i] = __ldcg(&recs[s].x);
+          cy[i] = __ldcg(&recs[s].y);
+          cid[i] = __ldcg(&recs[s].id);
+        } else {
+          const double2 cv = __ldcg(B.Lxy[pin] + w[i]);
+          cx[i] = cv.x;
+          cy[i] = cv.y;
+          cid[i] = __ldcg(&B.Lis[pin][w[i]].x);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      const uint32_t s = g0 + i * 32 + lane;
+      if (s < hi && w[i] != NONE) {
+        const uint32_t ns = s + wbase + wpre[i];
+        Route r;
+        r.ax = ax[i];
+        r.ay = ay[i];
+        r.cx = cx[i];
+        r.cy = cy[i];
+        r.bx = bx[i];
+        r.by = by[i];
+        r.cid = cid[i];
+        r.ns = ns;
+        r.flags = RT_SPLIT | (s < Slo ? RT_LOWER : 0u);
+        r.pad = 0;
         B.route[s] = r;
-        write_heads(B, pin, pout, r, s);
-        rec_clear(B.Sd[sout] + ns, B.Srec[sout] + ns);
-        if (r.flags & RT_SPLIT) rec_clear(B.Sd[sout] + ns + 1, B.Srec[sout] + ns + 1);
-        ns += (r.flags & RT_SPLIT) ? 2u : 1u;
+        Ox[ns + 1] = r.cx;
+        Oy[ns + 1] = r.cy;
+        Oid[ns + 1] = r.cid;
+        Wout[ns + 1] = NONE;
+        Sdo[ns] = 0ull;
+        Sdo[ns + 1] = 0ull;
       }
     }
     running += total;
@@ -513,13 +646,13 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   return true;
 }
 
-constexpr uint32_t ROUND_TARGET = 2 * LIVE_T;  // live points per active CTA before CTAs retire
+constexpr uint32_t ROUND_TARGET = 4 * RCTHREADS;  // live points per active CTA before CTAs retire
 
 __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RoundSmem& sm = *reinterpret_cast<RoundSmem*>(smem_raw);
   __shared__ uint32_t s_ws[RW + 1];
-  __shared__ uint32_t s_off;
+  __shared__ uint32_t s_off, s_coff;
   __shared__ uint32_t s_pref[MAX_RUNS + 1];
   Ctl* c = B.ctl;
   pdl_wait();  // round 1 (K3) is complete and visible
@@ -533,6 +666,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   const uint32_t target = min(ROUND_TARGET, q);
   uint32_t P = gridDim.x;
   bool recs_smem = false;  // this round's input records live in this CTA's smem
+  bool prev_small = true;  // the previous round used a small table (records in Srec)
   uint32_t kbase = 0;      // live tiles this CTA consumed in earlier rounds
   if (blockIdx.x == 0 && threadIdx.x == 0) c->mark[5] = globaltimer_ns() - c->t0_ns;
   unsigned long long t_table = 0, t_points = 0;  // CTA 0 phase timestamps
@@ -561,7 +695,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     uint32_t Sn, Slon;
     if (small) {
       table_small(B, sm, S, Slo, pin, pout, sin, recs_smem, s_ws, Sn, Slon);
-    } else if (!table_large(B, S, Slo, pin, pout, sin, sout, P, s_ws, Sn, Slon)) {
+    } else if (!table_large(B, S, Slo, pin, pout, sin, sout, P, prev_small, s_ws, Sn, Slon)) {
       return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) t_table = globaltimer_ns();
@@ -586,7 +720,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
         __syncthreads();
       }
     }
-    if (threadIdx.x == 0) s_off = 0;
+    if (threadIdx.x == 0) s_off = s_coff = 0;
     __syncthreads();
 
     // ---- point phase: virtual range [lo, hi) of the live set -> run j ----
@@ -705,17 +839,23 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
             if (lower) lowm |= 1u << u;
           }
         }
+        uint32_t candm = 0;
         if (small) {
           contend_tile<KR_U>(sm.db, sm.rec, keepm, px, py, pd, pid, pseg, lowm);
         } else {
-          // large table: fire-and-forget max of the distance bits; the winners
-          // are identified after the barrier (winner pass below)
+          // large table: max of the distance bits in the global slot; a
+          // survivor that reached the running maximum is listed for the
+          // winner pass after the barrier
 #pragma unroll
-          for (int u = 0; u < KR_U; ++u)
-            if ((keepm >> u) & 1u)
-              atomicMax(Sd + pseg[u], (unsigned long long)__double_as_longlong(pd[u]));
+          for (int u = 0; u < KR_U; ++u) {
+            if ((keepm >> u) & 1u) {
+              const unsigned long long db = (unsigned long long)__double_as_longlong(pd[u]);
+              if (db >= atomicMax(Sd + pseg[u], db)) candm |= 1u << u;
+            }
+          }
         }
-        run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase);
+        run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase, pd, candm, &s_coff,
+                         small ? nullptr : B.Lc);
       }
     }
     __syncthreads();
@@ -732,23 +872,49 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     if (threadIdx.x == 0 && r == c->tl_round) B.dbg[blockIdx.x] = globaltimer_ns() - c->t0_ns;
     rounds_barrier(c, P);
     if (!small) {
-      // winner pass: every survivor of this CTA (its run, still hot in L2)
-      // recomputes its distance against its new segment's base line -- the
-      // same RN operations as in routing, so bit-identical -- and the ones at
-      // the slot maximum settle the comparator's ties under the record lock
-      const double* Hx = B.Tx[pout];
-      const double* Hy = B.Ty[pout];
-      const uint32_t cnt = *(volatile uint32_t*)&s_off;
-      for (uint32_t e = threadIdx.x; e < cnt; e += RTPB) {
-        const double2 v = __ldcg(Oxy + obase + e);
-        const uint2 is = __ldcg(Ois + obase + e);
-        const uint32_t t = is.y, t1 = t + 1 == Sn ? 0u : t + 1;
-        const double d = outward_e(make_edge(__ldcg(Hx + t), __ldcg(Hy + t), __ldcg(Hx + t1),
-                                             __ldcg(Hy + t1)), v.x, v.y);
-        if ((unsigned long long)__double_as_longlong(d) == __ldcg(Sd + t)) {
+      // winner pass over this CTA's contenders (listed in its run's slice of
+      // Lc, still hot in L2): the ones whose distance equals their segment's
+      // final maximum claim its winner slot; exact ties settle the full
+      // comparator with a compare-and-swap loop over live-set positions
+      constexpr int WU = 4;
+      uint32_t* Wout = B.Wn[sout];
+      const LiveCand* Oc = B.Lc + obase;
+      const uint32_t cnt = *(volatile uint32_t*)&s_coff;
+      for (uint32_t e0 = threadIdx.x; e0 < cnt; e0 += RTPB * WU) {
+        LiveCand cv[WU];
+        unsigned long long mx[WU];
+#pragma unroll
+        for (int u = 0; u < WU; ++u) {
+          const uint32_t e = e0 + u * RTPB;
+          cv[u].seg = NONE;
+          if (e < cnt) {
+            const uint4 raw = __ldcg(reinterpret_cast<const uint4*>(Oc + e));
+            cv[u].d = __hiloint2double((int)raw.y, (int)raw.x);
+            cv[u].pos = raw.z;
+            cv[u].seg = raw.w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < WU; ++u) mx[u] = cv[u].seg != NONE ? __ldcg(Sd + cv[u].seg) : 0ull;
+#pragma unroll
+        for (int u = 0; u < WU; ++u) {
+          if (cv[u].seg == NONE || (unsigned long long)__double_as_longlong(cv[u].d) != mx[u]) continue;
+          uint32_t cur = atomicCAS(Wout + cv[u].seg, NONE, cv[u].pos);
+          if (cur == NONE) continue;
+          // a tie on the distance: the full comparator (hull.cpp:171-179)
           Cand me;
-          me.d = d; me.x = v.x; me.y = v.y; me.id = is.x; me.pos = 0;
-          rec_update<false>(Srec + t, me, t < Slon);
+          const double2 mv = __ldcg(Oxy + cv[u].pos);
+          me.d = cv[u].d; me.x = mv.x; me.y = mv.y; me.id = __ldcg(&Ois[cv[u].pos].x); me.pos = 0;
+          const bool lower = cv[u].seg < Slon;
+          while (cur != NONE) {
+            Cand o;
+            const double2 ov = __ldcg(Oxy + cur);
+            o.d = me.d; o.x = ov.x; o.y = ov.y; o.id = __ldcg(&Ois[cur].x); o.pos = 0;
+            if (!cand_better(me, o, lower)) break;
+            const uint32_t prev = atomicCAS(Wout + cv[u].seg, cur, cv[u].pos);
+            if (prev == cur) break;
+            cur = prev;
+          }
         }
       }
       rounds_barrier(c, P);
@@ -773,6 +939,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     m = mn;
     nruns = P;
     recs_smem = keep_smem;
+    prev_small = small;
     if (mn == 0 || r + 1 > n) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         c->round = r;

@@ -169,10 +169,13 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
     o_ty[p] = take(8 * S);
     o_tid[p] = take(4 * S);
   }
+  size_t o_wn[3];
   for (int p = 0; p < 3; ++p) {
     o_sd[p] = take(8 * S);
-    o_sw[p] = take(sizeof(SlotRec) * S);
+    o_sw[p] = take(sizeof(SlotRec) * NSLOT);  // records exist for small tables only
+    o_wn[p] = take(4 * S);
   }
+  const size_t o_lc = take(sizeof(LiveCand) * LN);
   const size_t o_route = take(sizeof(Route) * S);
   CK(cudaMalloc(&ws->arena, off));
   char* a = (char*)ws->arena;
@@ -199,7 +202,9 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   for (int p = 0; p < 3; ++p) {
     B.Sd[p] = (unsigned long long*)(a + o_sd[p]);
     B.Srec[p] = (SlotRec*)(a + o_sw[p]);
+    B.Wn[p] = (uint32_t*)(a + o_wn[p]);
   }
+  B.Lc = (LiveCand*)(a + o_lc);
   B.route = (Route*)(a + o_route);
   B.s_cap = (uint32_t)std::min<uint64_t>(s_cap, 0xFFFFFFF0ull);
   return ws;
