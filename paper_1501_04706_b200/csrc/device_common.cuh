@@ -146,6 +146,14 @@ SH_DEV unsigned long long globaltimer_ns() {
 SH_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 SH_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// The value, hidden from the optimiser: keeps it from unswitching code on a
+// data-dependent index with few possible values (e.g. computing a point's
+// route for both chains and selecting afterwards).
+SH_DEV uint32_t opaque_u32(uint32_t v) {
+  asm("" : "+r"(v));
+  return v;
+}
+
 SH_DEV uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

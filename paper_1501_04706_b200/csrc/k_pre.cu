@@ -396,8 +396,12 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   // One tile; FULLT: cnt == T (no bounds checks anywhere).  All decisions are
   // bitwise predicates; the rare candidate updates sit behind one
   // warp-uniform branch.
-  auto tile = [&](auto fullt, int s, uint32_t first, uint32_t cnt) {
+  // QK: 1 = the 4-corner quadrilateral, 2 = a degenerate one (<= 3 edges),
+  // 0 = no filter -- a compile-time choice, so the hot path carries no
+  // predicated-off arithmetic of the other variants
+  auto tile = [&](auto fullt, auto qk, int s, uint32_t first, uint32_t cnt) {
     constexpr bool FULLT = decltype(fullt)::value;
+    constexpr int QK = decltype(qk)::value;
     const double* xs = R.xs + s * Cfg2::T;
     const double* ys = R.ys + s * Cfg2::T;
     const uint32_t* is = R.is + s * Cfg2::T;
@@ -447,14 +451,14 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
       cl[q] = xprod(E01.ex, E01.ey, dxL, dyL);         // cross(P0, Pr, p)
       du[q] = -xprod(E10.ex, E10.ey, dxR, dyR);        // outward_distance(Pr, P0, p)
       bool inside = false;
-      if (quad4) {  // hull.cpp:80-90: discard iff cross > 0 for every edge
+      if (QK == 1) {  // hull.cpp:80-90: discard iff cross > 0 for every edge
         const double dxB = __dsub_rn(x, cxB), dyB = __dsub_rn(y, cyB);
         const double dxT = __dsub_rn(x, cxT), dyT = __dsub_rn(y, cyT);
         inside = (xprod(Q[0].ex, Q[0].ey, dxL, dyL) > 0.0) &
                  (xprod(Q[1].ex, Q[1].ey, dxB, dyB) > 0.0) &
                  (xprod(Q[2].ex, Q[2].ey, dxR, dyR) > 0.0) &
                  (xprod(Q[3].ex, Q[3].ey, dxT, dyT) > 0.0);
-      } else if (filt) {  // degenerate quadrilateral (3 distinct corners)
+      } else if (QK == 2) {  // degenerate quadrilateral (3 distinct corners)
         inside = true;
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq)
@@ -504,12 +508,20 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
     if (a0.d > ad0) atomicMax(&s_dmax[0], (unsigned long long)__double_as_longlong(a0.d));
     if (a1.d > ad1) atomicMax(&s_dmax[1], (unsigned long long)__double_as_longlong(a1.d));
   };
-  stream_input(R, n, X, Y, I, nullptr, SHB_K2_REVERSE != 0, [&](int s, uint32_t first, uint32_t cnt) {
-    if (cnt == (uint32_t)Cfg2::T)
-      tile(std::true_type{}, s, first, cnt);
-    else
-      tile(std::false_type{}, s, first, cnt);
-  });
+  auto pass = [&](auto qk) {
+    stream_input(R, n, X, Y, I, nullptr, SHB_K2_REVERSE != 0, [&](int s, uint32_t first, uint32_t cnt) {
+      if (cnt == (uint32_t)Cfg2::T)
+        tile(std::true_type{}, qk, s, first, cnt);
+      else
+        tile(std::false_type{}, qk, s, first, cnt);
+    });
+  };
+  if (quad4)
+    pass(std::integral_constant<int, 1>{});
+  else if (filt)
+    pass(std::integral_constant<int, 2>{});
+  else
+    pass(std::integral_constant<int, 0>{});
 
   // block reduction of the two chains' farthest candidates
   __shared__ Cand s_a[2][MAXW];

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
         const uint32_t uw = ((h ? bits.w : bits.z) >> lane) & 1u;
         bool lower = false;
         const bool keep =
-            route_point<false>(s_rt + (lw ? 0 : 1), px[q], py[q], pid[q], pd[q], pseg[q], lower);
+            route_point<false>(s_rt + opaque_u32(lw ^ 1u), px[q], py[q], pid[q], pd[q], pseg[q], lower);
         keepm |= (uint32_t)((lw | uw) & keep) << q;
         lowm |= lw << q;
       }

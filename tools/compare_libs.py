@@ -1,5 +1,5 @@
 """Time the pipeline with several library builds in ONE process per build, same box.
-    python tools/compare_libs.py build_var/lib_*.so"""
+    [KIND=uniform|disk|circle N=2e7] python tools/compare_libs.py build_var/lib_*.so"""
 import os, subprocess, sys, json
 code = r'''
 import os, sys, statistics, json
@@ -7,7 +7,14 @@ sys.path.insert(0, os.getcwd())
 import torch
 from paper_1501_04706_b200 import dataio, hull
 n = int(float(os.environ.get("N", "2e7")))
-x, y = dataio.gen_uniform_device(n, 1)
+kind = os.environ.get("KIND", "uniform")
+if kind == "uniform":
+    x, y = dataio.gen_uniform_device(n, 1)
+elif kind == "disk":
+    x, y = dataio.gen_disk_device(n, 1)
+else:
+    hx, hy = dataio.gen_circle(n, 1)
+    x, y = torch.from_numpy(hx).cuda(), torch.from_numpy(hy).cuda()
 torch.cuda.synchronize()
 ks = []
 for i in range(12):
