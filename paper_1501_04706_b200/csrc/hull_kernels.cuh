@@ -157,7 +157,7 @@ struct StatRec {
 
 // Device-resident control block.  The host writes it once per call and
 // reads it once at the end; all round bookkeeping stays on the device.
-struct Ctl {
+struct __align__(16) Ctl {
   uint32_t status;
   uint32_t round;       // refinement rounds completed
   uint32_t S_cur;       // segments after `round`
@@ -223,5 +223,9 @@ struct Bufs {
   LiveCand* Lc;
   Route* route;
 };
+// The control block and the round stats are contiguous in the arena, so ONE
+// device-to-host copy of {Ctl; StatRec[STATS_EAGER]} ends a call.
+constexpr size_t HOST_RES_STATS = (sizeof(Ctl) + 15) / 16 * 16;
+constexpr size_t HOST_RES_BYTES = HOST_RES_STATS + sizeof(StatRec) * STATS_EAGER;
 
 }  // namespace shb

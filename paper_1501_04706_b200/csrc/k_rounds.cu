@@ -963,6 +963,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
 
 __global__ void k5_emit(Bufs B, double* ox, double* oy, long long* oidx, uint64_t cap) {
   const Ctl* c = B.ctl;
+  pdl_wait();  // launched early (programmatic serialisation): the rounds are done
   if (c->status != ST_DONE) return;
   const uint32_t par = c->round & 1u;
   const uint32_t h = c->S_cur;
@@ -1035,7 +1036,20 @@ cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s) {
 
 void launch_k5(const Bufs& B, double* ox, double* oy, long long* oidx, uint64_t cap,
                cudaStream_t s) {
+#ifdef SHB_K5_PLAIN
   k5_emit<<<16, 256, 0, s>>>(B, ox, oy, oidx, cap);
+  return;
+#endif
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k5_emit, B, ox, oy, oidx, cap);
 }
 
 }  // namespace shb

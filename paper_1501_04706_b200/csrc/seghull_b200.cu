@@ -78,8 +78,9 @@ struct Workspace {
   void* stage = nullptr;
   Bufs B{};
   uint32_t* epoch = nullptr;
-  Ctl* h_ctl = nullptr;        // pinned
-  StatRec* h_stats = nullptr;  // pinned
+  unsigned char* h_res = nullptr;  // pinned: {Ctl; StatRec[STATS_EAGER]}, one copy per call
+  Ctl* h_ctl = nullptr;            // = h_res
+  StatRec* h_stats = nullptr;      // pinned, all rounds
   cudaEvent_t ev[8] = {};
   size_t tiles_cap = 0;
   int stream_grid = 0, rounds_grid = 0;
@@ -90,7 +91,7 @@ struct Workspace {
     cudaSetDevice(device);
     if (arena) cudaFree(arena);
     if (stage) cudaFree(stage);
-    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_res) cudaFreeHost(h_res);
     if (h_stats) cudaFreeHost(h_stats);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -130,7 +131,8 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   DeviceInfo& di = device_info(device);
   CK(cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking));
   for (auto& e : ws->ev) CK(cudaEventCreate(&e));
-  CK(cudaMallocHost((void**)&ws->h_ctl, sizeof(Ctl)));
+  CK(cudaMallocHost((void**)&ws->h_res, HOST_RES_BYTES));
+  ws->h_ctl = reinterpret_cast<Ctl*>(ws->h_res);
   CK(cudaMallocHost((void**)&ws->h_stats, sizeof(StatRec) * STATS_CAP));
 
   const uint64_t N = std::max<uint64_t>(n_cap, 64), S = std::max<uint64_t>(s_cap, 64);
@@ -147,10 +149,9 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
     off = align_up(off + bytes, 256);
     return o;
   };
-  const size_t o_ctl = take(sizeof(Ctl));
+  const size_t o_ctl = take(HOST_RES_STATS + sizeof(StatRec) * STATS_CAP);  // Ctl, then the stats
   const size_t o_epoch = take(sizeof(uint32_t));
   const size_t o_k1 = take(sizeof(K1Partial) * ws->stream_grid);
-  const size_t o_stats = take(sizeof(StatRec) * STATS_CAP);
   const size_t o_blk = take(sizeof(uint32_t) * 2 * MAX_ROUND_BLOCKS);
   const size_t o_dbg = take(sizeof(unsigned long long) * MAX_ROUND_BLOCKS);
   const size_t o_tiles = take(sizeof(unsigned long long) * ws->tiles_cap);
@@ -186,7 +187,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   const uint32_t one = 1;
   CK(cudaMemcpy(ws->epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
   B.k1part = (K1Partial*)(a + o_k1);
-  B.stats = (StatRec*)(a + o_stats);
+  B.stats = (StatRec*)(a + o_ctl + HOST_RES_STATS);
   B.blk_cnt = (uint32_t*)(a + o_blk);
   B.dbg = (unsigned long long*)(a + o_dbg);
   B.tile_status = (unsigned long long*)(a + o_tiles);
@@ -353,17 +354,22 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
     CK(cudaGetLastError());
     out.launches += 1;
   }
-  CK(cudaMemcpyAsync(ws.h_ctl, B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  // ONE copy: the control block and the first round stats
+  CK(cudaMemcpyAsync(ws.h_res, B.ctl, HOST_RES_BYTES, cudaMemcpyDeviceToHost, st));
   const bool want_stats = res.stats && res.stats_cap && !(rq.flags & SH_NO_STATS);
-  if (want_stats)
-    CK(cudaMemcpyAsync(ws.h_stats, B.stats, sizeof(StatRec) * STATS_EAGER,
-                       cudaMemcpyDeviceToHost, st));
   if (timings) CK(cudaEventRecord(ws.ev[6], st));
   CK(cudaStreamSynchronize(st));
+  if (want_stats)
+    std::memcpy(ws.h_stats, ws.h_res + HOST_RES_STATS,
+                sizeof(StatRec) * std::min<uint64_t>(ws.h_ctl->round, STATS_EAGER));
 
   const Ctl& c = *ws.h_ctl;
   g_last_tl[0] = c.tl_n;
   for (uint32_t i = 0; i < c.tl_n && i < 32; ++i) g_last_tl[i + 1] = c.tl[i];
+  if (g_trace_round == 255) {  // debug: the kernel marks instead (t0 = K1 start)
+    g_last_tl[0] = 8;
+    for (int i = 0; i < 8; ++i) g_last_tl[i + 1] = c.mark[i];
+  }
   if (g_trace_round) {
     g_last_ctas.resize(MAX_ROUND_BLOCKS);
     CK(cudaMemcpy(g_last_ctas.data(), B.dbg, sizeof(unsigned long long) * MAX_ROUND_BLOCKS,

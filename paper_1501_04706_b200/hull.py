@@ -17,6 +17,7 @@ Every compute call goes through libseghull_b200.so; there is no CPU path.
 """
 from __future__ import annotations
 
+import collections.abc
 import ctypes
 import enum
 import threading
@@ -178,6 +179,9 @@ class KernelTimings:
     d2h_ms: float = 0.0
 
 
+_ZERO_KT = KernelTimings()
+
+
 def _prepare(x, y, ids):
     if isinstance(x, np.ndarray):
         x = np.ascontiguousarray(x, dtype=np.float64)
@@ -212,9 +216,54 @@ def _stats_buffer(cap: int):
     return buf
 
 
+class RoundList(collections.abc.Sequence):
+    """Per-round records of one call, parsed on first access from a copy of the
+    library's sh_round_stat rows: kind 0 = SegmentStats (hull.hpp:35-40),
+    1 = device time at the end of each round (ms since K1 started),
+    2 = (table phase end, point phase end, round end) in ms."""
+    __slots__ = ("_raw", "_kind", "_items")
+
+    def __init__(self, raw: bytes = b"", kind: int = 0):
+        self._raw = raw
+        self._kind = kind
+        self._items = None
+
+    def _get(self) -> list:
+        if self._items is None:
+            a = np.frombuffer(self._raw, dtype=np.uint64).reshape(-1, 7).tolist()
+            if self._kind == 0:
+                self._items = [SegmentStats(r[0], r[1], r[2], r[3]) for r in a]
+            elif self._kind == 1:
+                self._items = [r[4] * 1e-6 for r in a]
+            else:
+                self._items = [(r[5] * 1e-6, r[6] * 1e-6, r[4] * 1e-6) for r in a]
+        return self._items
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __len__(self) -> int:
+        return len(self._raw) // _ROW
+
+    def __eq__(self, other) -> bool:
+        return list(self) == list(other)
+
+    def __repr__(self) -> str:
+        return repr(self._get())
+
+
+_ROW = ctypes.sizeof(_lib.sh_round_stat)
+
+
+_ZERO_PH = PhaseTimings()
+
+
 def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, stats_cap):
     L = _lib.load()
-    req = _lib.sh_hull_request()
+    io = getattr(_tls, "io", None)  # per-thread request/result structs, reused
+    if io is None:
+        io = _tls.io = (_lib.sh_hull_request(), _lib.sh_hull_result())
+    req, res = io
     req.x = px
     req.y = py
     req.n = n
@@ -224,7 +273,6 @@ def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, st
     req.device = int(device)
     req.stream = stream
     st = _stats_buffer(stats_cap)
-    res = _lib.sh_hull_result()
     res.idx = oi
     res.x = ox
     res.y = oy
@@ -235,16 +283,16 @@ def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, st
     if rc != 0:
         _raise(rc, res.err.decode(errors="replace"))
     nst = min(int(res.rounds), stats_cap)
-    sts = [SegmentStats(int(st[i].iteration), int(st[i].segments), int(st[i].points_remaining),
-                        int(st[i].points_removed)) for i in range(nst)]
-    ends = [st[i].end_ns * 1e-6 for i in range(nst)]
-    phases = [(st[i].table_ns * 1e-6, st[i].points_ns * 1e-6, st[i].end_ns * 1e-6)
-              for i in range(nst)]
-    ph = PhaseTimings(res.phases.pre_ms, res.phases.split_ms, res.phases.recurse_ms,
-                      res.phases.total_ms)
-    k = res.kernels
-    kt = KernelTimings(k.h2d_ms, k.extremes_ms, k.filter_ms, k.first_round_ms, k.rounds_ms,
-                       k.d2h_ms)
+    raw = ctypes.string_at(ctypes.addressof(st), nst * _ROW) if nst else b""
+    sts, ends, phases = RoundList(raw, 0), RoundList(raw, 1), RoundList(raw, 2)
+    if flags & _lib.SH_PHASE_TIMINGS:
+        ph = PhaseTimings(res.phases.pre_ms, res.phases.split_ms, res.phases.recurse_ms,
+                          res.phases.total_ms)
+        k = res.kernels
+        kt = KernelTimings(k.h2d_ms, k.extremes_ms, k.filter_ms, k.first_round_ms, k.rounds_ms,
+                           k.d2h_ms)
+    else:
+        ph, kt = _ZERO_PH, _ZERO_KT
     return res, sts, ph, kt, (ends, phases)
 
 

@@ -38,7 +38,7 @@ for _ in range(reps):
         k = L.sh_b200_debug_last_timeline(buf, 32)
         ts = [buf[i] / 1e3 for i in range(k)]
         if trace == 255:
-            print("   kernel marks (us): K1 start 0, K1 end %.1f | K2 start %.1f end %.1f | K3 start %.1f end %.1f | KR start %.1f" % tuple(ts[1:7]))
+            print("   kernel marks (us): K1 end %.1f | K2 start %.1f end %.1f | K3 start %.1f end %.1f | KR start %.1f end %.1f" % tuple(ts[0:7]))
         else:
             print(f"   trace round {trace} (us since K1 start; tile wait begin/end):", [round(t, 2) for t in ts])
         cb = (ctypes.c_ulonglong * 1024)()
