@@ -646,6 +646,213 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Solo tail: once a single CTA is left with a small table and a live set that
+// fits its shared memory, it runs the remaining rounds with everything in
+// shared memory -- live points (ping-pong), head table, route table and
+// farthest records -- touching global memory only for the round stats and,
+// at the end, the final head table.  The ring's storage is reused.
+constexpr uint32_t SOLO_CAP = 2304;  // live points per ping-pong buffer
+static_assert(2 * SOLO_CAP + NSLOT <= (uint32_t)(LIVE_NS * LIVE_T), "solo tail does not fit the ring");
+static_assert(SMALL_S <= RTPB && 2 * SMALL_S <= NSLOT, "solo table: one segment per thread");
+
+struct SoloState {
+  uint32_t r, S, Slo, m, nruns;
+};
+
+// Returns true when the call is finished (control block written), false when
+// the table outgrew SMALL_S: the state is then exported to global memory (one
+// run, records in Srec) and the caller continues with the grid-wide rounds.
+SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, bool recs_smem,
+                        uint32_t* s_ws, uint32_t* s_pref, uint32_t* s_off) {
+  Ctl* c = B.ctl;
+  const uint32_t tid = threadIdx.x, q = B.run_q, n = B.n;
+  double2* const buf_xy = &sm.lxy[0][0];
+  uint2* const buf_is = &sm.lis[0][0];
+  double2* const hxy = buf_xy + 2 * SOLO_CAP;  // head table (x, y)
+  uint2* const hid = buf_is + 2 * SOLO_CAP;    // head ids (.x)
+  uint32_t r = st.r, S = st.S, Slo = st.Slo, m = st.m;
+  const unsigned long long t0 = *(volatile unsigned long long*)&c->t0_ns;
+  {  // ---- import: heads, records (unless already here), live set ----
+    const uint32_t pin = (r - 1) & 1u, sin = (r - 1) % 3u;
+    for (uint32_t s = tid; s < S; s += RTPB) {
+      hxy[s] = make_double2(__ldcg(B.Tx[pin] + s), __ldcg(B.Ty[pin] + s));
+      hid[s].x = __ldcg(B.Tid[pin] + s);
+      if (!recs_smem) {
+        sm.db[s] = __ldcg(B.Sd[sin] + s);
+        const SlotRec* g = B.Srec[sin] + s;
+        sm.rec[s].d = __ldcg(&g->d);
+        sm.rec[s].x = __ldcg(&g->x);
+        sm.rec[s].y = __ldcg(&g->y);
+        sm.rec[s].id = __ldcg(&g->id);
+        sm.rec[s].lock = 0u;
+      }
+    }
+    const uint32_t nruns = st.nruns;
+    uint32_t tot;
+    for (uint32_t j0 = 0; j0 < nruns; j0 += RTPB) {
+      const uint32_t j = j0 + tid;
+      uint32_t v = j < nruns ? (nruns == 1 ? m : __ldcg(B.run_cnt[pin] + j)) : 0u;
+      v += v & 1u;
+      const uint32_t base0 = j0 ? s_pref[j0] : 0u;
+      const uint32_t ex = block_exclusive_scan(v, s_ws, &tot);
+      if (j < nruns) s_pref[j] = base0 + ex;
+      if (tid == 0) s_pref[min(j0 + RTPB, nruns)] = base0 + tot;
+      __syncthreads();
+    }
+    const uint32_t Mp = s_pref[nruns];
+    for (uint32_t v = tid; v < Mp; v += RTPB) {
+      uint32_t a0 = 0, a1 = nruns;
+      while (a1 - a0 > 1) {
+        const uint32_t mid = (a0 + a1) >> 1;
+        if (s_pref[mid] <= v) a0 = mid; else a1 = mid;
+      }
+      const uint32_t phys = a0 * q + (v - s_pref[a0]);
+      buf_xy[v] = __ldcg(B.Lxy[pin] + phys);
+      buf_is[v] = __ldcg(B.Lis[pin] + phys);
+    }
+    m = Mp;  // entries of buffer 0, pads (segment NONE) included
+    __syncthreads();
+  }
+  uint32_t cur = 0;
+  while (true) {
+    const uint32_t pout = r & 1u;
+    // ---- table: routes from heads + records, then the new heads in place ----
+    uint32_t Sn, Slon;
+    {
+      uint32_t total;
+      const uint32_t s = tid;  // S <= SMALL_S <= RTPB
+      const bool split = s < S && sm.rec[s].id != NONE;
+      const uint32_t pre = block_exclusive_scan(split ? 1u : 0u, s_ws, &total);
+      const uint32_t lower_splits = (uint32_t)__syncthreads_count(split && s < Slo);
+      if (s < S) {
+        Route rr;
+        const double2 a = hxy[s], b = hxy[s + 1 == S ? 0u : s + 1];
+        rr.ax = a.x; rr.ay = a.y; rr.bx = b.x; rr.by = b.y;
+        rr.cx = split ? sm.rec[s].x : 0.0;
+        rr.cy = split ? sm.rec[s].y : 0.0;
+        rr.cid = split ? sm.rec[s].id : NONE;
+        rr.ns = s + pre;
+        rr.flags = (split ? RT_SPLIT : 0u) | (s < Slo ? RT_LOWER : 0u);
+        rr.pad = hid[s].x;  // A's id, for the new head table
+        sm.rt[s] = rr;
+      }
+      Sn = S + total;
+      Slon = Slo + lower_splits;
+      __syncthreads();
+      if (s < S) {
+        const Route rr = sm.rt[s];
+        hxy[rr.ns] = make_double2(rr.ax, rr.ay);
+        hid[rr.ns].x = rr.pad;
+        if (rr.flags & RT_SPLIT) {
+          hxy[rr.ns + 1] = make_double2(rr.cx, rr.cy);
+          hid[rr.ns + 1].x = rr.cid;
+        }
+      }
+      for (uint32_t t = tid; t < Sn; t += RTPB) rec_clear(&sm.db[t], &sm.rec[t]);
+      if (tid == 0) *s_off = 0;
+      __syncthreads();
+    }
+    const unsigned long long t_table = globaltimer_ns();
+    // ---- points: route, keep, contend, append to the other buffer ----
+    const double2* ixy = buf_xy + cur * SOLO_CAP;
+    const uint2* iis = buf_is + cur * SOLO_CAP;
+    double2* oxy = buf_xy + (cur ^ 1u) * SOLO_CAP;
+    uint2* ois = buf_is + (cur ^ 1u) * SOLO_CAP;
+    for (uint32_t i0 = 0; i0 < m; i0 += 2 * RTPB) {
+      double px[2], py[2], pd[2];
+      uint32_t pid[2], pseg[2];
+      uint32_t keepm = 0, lowm = 0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t i = i0 + u * RTPB + tid;
+        px[u] = py[u] = pd[u] = 0.0;
+        pid[u] = 0;
+        pseg[u] = 0;
+        if (i < m) {
+          const double2 v = ixy[i];
+          const uint2 is = iis[i];
+          if (is.y != NONE) {
+            bool lower = false;
+            px[u] = v.x;
+            py[u] = v.y;
+            pid[u] = is.x;
+            if (route_point<false>(sm.rt + is.y, v.x, v.y, is.x, pd[u], pseg[u], lower)) keepm |= 1u << u;
+            if (lower) lowm |= 1u << u;
+          }
+        }
+      }
+      contend_tile<2>(sm.db, sm.rec, keepm, px, py, pd, pid, pseg, lowm);
+      run_append<2>(keepm, px, py, pid, pseg, s_off, oxy, ois, 0u);
+    }
+    __syncthreads();
+    const uint32_t mn = *(volatile uint32_t*)s_off;
+    if (tid == 0 && r <= (uint32_t)STATS_CAP) {
+      StatRec sr;
+      sr.segments = Sn;
+      sr.points_remaining = Sn + mn;
+      sr.points_removed = (S + st.m) - (Sn + mn);
+      sr.pad = 0;
+      const unsigned long long now = globaltimer_ns();
+      sr.end_ns = now - t0;
+      sr.table_ns = t_table - t0;
+      sr.points_ns = now - t0;
+      B.stats[r - 1] = sr;
+    }
+    const bool done = mn == 0 || r + 1 > n;
+    if (done || Sn > (uint32_t)SMALL_S) {
+      // ---- export: the head table (+ records and live set to continue) ----
+      for (uint32_t t = tid; t < Sn; t += RTPB) {
+        const double2 h = hxy[t];
+        B.Tx[pout][t] = h.x;
+        B.Ty[pout][t] = h.y;
+        B.Tid[pout][t] = hid[t].x;
+      }
+      if (done) {
+        if (tid == 0) {
+          c->round = r;
+          c->S_cur = Sn;
+          c->Slo_cur = Slon;
+          c->m_cur = mn;
+          c->nruns = 1;
+          c->status = mn == 0 ? ST_DONE : ST_INTERNAL;  // hull.cpp:265-267
+          c->mark[6] = globaltimer_ns() - t0;
+          __threadfence();
+        }
+        return true;
+      }
+      const uint32_t sout = r % 3u;
+      for (uint32_t t = tid; t < Sn; t += RTPB) {
+        B.Sd[sout][t] = sm.db[t];
+        SlotRec* g = B.Srec[sout] + t;
+        g->d = sm.rec[t].d;
+        g->x = sm.rec[t].x;
+        g->y = sm.rec[t].y;
+        g->id = sm.rec[t].id;
+        g->lock = 0u;
+      }
+      for (uint32_t t = tid; t < mn + (mn & 1u); t += RTPB) {
+        B.Lxy[pout][t] = t < mn ? oxy[t] : make_double2(0.0, 0.0);
+        B.Lis[pout][t] = t < mn ? ois[t] : make_uint2(NONE, NONE);
+      }
+      if (tid == 0) B.run_cnt[pout][0] = mn;
+      __syncthreads();
+      st.r = r + 1;
+      st.S = Sn;
+      st.Slo = Slon;
+      st.m = mn;
+      st.nruns = 1;
+      return false;
+    }
+    S = Sn;
+    Slo = Slon;
+    st.m = mn;  // real points of the next round (for points_removed)
+    m = mn;
+    cur ^= 1u;
+    ++r;
+  }
+}
+
 constexpr uint32_t ROUND_TARGET = 4 * RCTHREADS;  // live points per active CTA before CTAs retire
 
 __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
@@ -658,6 +865,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   pdl_wait();  // round 1 (K3) is complete and visible
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   uint32_t r = *(volatile uint32_t*)&c->round + 1;
+  const uint32_t trace_r = c->tl_round;  // debug timeline of CTA 0 in this round (0: off)
+#define KR_MARK()                                                               \
+  if (trace_r == r && blockIdx.x == 0 && threadIdx.x == 0 && c->tl_n < 32u)     \
+    c->tl[c->tl_n++] = globaltimer_ns() - c->t0_ns;
   uint32_t S = *(volatile uint32_t*)&c->S_cur;
   uint32_t Slo = *(volatile uint32_t*)&c->Slo_cur;
   uint32_t m = *(volatile uint32_t*)&c->m_cur;
@@ -689,6 +900,19 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       if (blockIdx.x >= want) return;
       P = want;
     }
+    KR_MARK();  // round start
+    if (P == 1 && S <= (uint32_t)SMALL_S && m + nruns <= SOLO_CAP) {
+      SoloState ss{r, S, Slo, m, nruns};
+      if (solo_rounds(B, sm, ss, recs_smem, s_ws, s_pref, &s_off)) return;
+      r = ss.r;
+      S = ss.S;
+      Slo = ss.Slo;
+      m = ss.m;
+      nruns = ss.nruns;
+      recs_smem = false;
+      prev_small = true;
+      continue;
+    }
     const uint32_t pin = (r - 1) & 1u, pout = r & 1u;
     const uint32_t sin = (r - 1) % 3u, sout = r % 3u, sres = (r + 1) % 3u;
     const bool small = S <= (uint32_t)SMALL_S;
@@ -699,6 +923,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) t_table = globaltimer_ns();
+    KR_MARK();  // table done
     // clear round r+1's global farthest slots (at most 2 Sn segments) when
     // round r+1 will use a small table; a large table clears its own slots
     if (Sn <= (uint32_t)SMALL_S) {
@@ -722,6 +947,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     }
     if (threadIdx.x == 0) s_off = s_coff = 0;
     __syncthreads();
+    KR_MARK();  // slots cleared, run prefix built
 
     // ---- point phase: virtual range [lo, hi) of the live set -> run j ----
     // The runs are read as one virtual range (padded counts, all even); each
@@ -859,6 +1085,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       }
     }
     __syncthreads();
+    KR_MARK();  // point loop done
     if (use_tma) kbase += ntl;  // stage uses so far (phase parity of the ring)
     if (threadIdx.x == 0 && (s_off & 1u)) {  // pad the run to an even length
       Oxy[obase + s_off] = make_double2(0.0, 0.0);
@@ -869,8 +1096,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     if (small && !keep_smem) flush_slots(sm.db, sm.rec, Sn, Slon, Sd, Srec);
     if (threadIdx.x == 0) B.run_cnt[pout][blockIdx.x] = s_off;
     if (blockIdx.x == 0 && threadIdx.x == 0) t_points = globaltimer_ns();
-    if (threadIdx.x == 0 && r == c->tl_round) B.dbg[blockIdx.x] = globaltimer_ns() - c->t0_ns;
+    if (threadIdx.x == 0 && r == trace_r) B.dbg[blockIdx.x] = globaltimer_ns() - c->t0_ns;
+    KR_MARK();  // slots flushed
     rounds_barrier(c, P);
+    KR_MARK();  // barrier passed
     if (!small) {
       // winner pass over this CTA's contenders (listed in its run's slice of
       // Lc, still hot in L2): the ones whose distance equals their segment's
@@ -920,6 +1149,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       rounds_barrier(c, P);
     }
 
+    KR_MARK();  // winner pass done
     // ---- close round r (every participating CTA computes the same) ----
     const uint32_t mn = P == 1 ? *(volatile uint32_t*)&s_off : sum_runs(B.run_cnt[pout], P, s_ws);
     if (blockIdx.x == 0 && threadIdx.x == 0 && r <= (uint32_t)STATS_CAP) {

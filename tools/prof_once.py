@@ -40,10 +40,12 @@ for _ in range(reps):
         if trace == 255:
             print("   kernel marks (us): K1 end %.1f | K2 start %.1f end %.1f | K3 start %.1f end %.1f | KR start %.1f end %.1f" % tuple(ts[0:7]))
         else:
-            print(f"   trace round {trace} (us since K1 start; tile wait begin/end):", [round(t, 2) for t in ts])
+            print(f"   trace round {trace} (us since K1 start: start, table, prefix, points, flush, barrier, [winner]):", [round(t, 2) for t in ts])
         cb = (ctypes.c_ulonglong * 1024)()
         L.sh_b200_debug_last_ctas(cb, 1024)
         ends = sorted(cb[i] / 1e3 for i in range(1024) if cb[i])
+        slow = sorted((cb[i] / 1e3, i) for i in range(1024) if cb[i])[-10:]
+        print("   slowest CTAs (end us, cta):", [(round(t, 1), i) for t, i in slow])
         if ends:
             import statistics
             print(f"   CTA point-phase ends: n={len(ends)} min {ends[0]:.1f} median {statistics.median(ends):.1f} max {ends[-1]:.1f} us; deciles",
