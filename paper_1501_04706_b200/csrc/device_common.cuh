@@ -58,10 +58,6 @@ SH_DEV bool lex_less(double ax, double ay, double bx, double by) {
 // (a segment is splittable iff its max d > 0, hull.cpp:190), so d == 0 with
 // id == NONE is the empty record.
 
-struct Cand {
-  double d, x, y;
-  uint32_t id, pos;
-};
 
 SH_DEV Cand empty_cand() {
   Cand c;
@@ -100,12 +96,79 @@ SH_DEV Cand shfl_xor_cand(const Cand& c, int m) {
   return o;
 }
 
+// Order-preserving integer key of a finite double under FP comparison: -0.0
+// and +0.0 compare equal, so both get the key of +0.0.  Integer compares of
+// keys are short-latency and branch-free, unlike chains of FP64 compares.
+SH_DEV unsigned long long fkey(double v) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  b = (b << 1) == 0ull ? 0ull : b;
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// cand_better on keys, branch-free (same order: candidates' d are > 0 or the
+// empty 0.0, whose bit patterns order like the values)
+SH_DEV bool cand_better_k(const Cand& a, const Cand& b, bool lower) {
+  const unsigned long long da = (unsigned long long)__double_as_longlong(a.d);
+  const unsigned long long db = (unsigned long long)__double_as_longlong(b.d);
+  const unsigned long long ax = fkey(a.x), bx = fkey(b.x), ay = fkey(a.y), by = fkey(b.y);
+  const bool xl = lower ? ax < bx : ax > bx, yl = lower ? ay < by : ay > by;
+  return (da > db) | ((da == db) & (xl | ((ax == bx) & (yl | ((ay == by) & (a.id < b.id))))));
+}
+
+// warp-wide minimum of a 64-bit key (two 32-bit redux steps)
+SH_DEV unsigned long long warp_min_u64(unsigned long long v) {
+  const uint32_t hi = (uint32_t)(v >> 32);
+  const uint32_t mh = __reduce_min_sync(FULL, hi);
+  const uint32_t ml = __reduce_min_sync(FULL, hi == mh ? (uint32_t)v : 0xFFFFFFFFu);
+  return ((unsigned long long)mh << 32) | ml;
+}
+
+// CTA-wide lexicographic argmin, per slot, of the key tuples the threads
+// offer (smaller is better at every level; invalid offers are skipped):
+// one warp min + one shared atomicMin per warp per level, and a barrier per
+// level -- no FP64 compare chains, no block-wide shuffles of records.
+// s_best[NSL][NK] is scratch; on return win[s] tells whether this thread's
+// tuple equals the slot's minimum (several threads only for equal tuples,
+// so the last key should make tuples unique) and s_best holds the minima
+// (all ~0 for a slot without offers).
+template <int NSL, int NK>
+SH_DEV void cta_lexmin(const unsigned long long (&key)[NSL][NK], const bool (&valid)[NSL],
+                       unsigned long long (*s_best)[NK], bool (&win)[NSL]) {
+  __syncthreads();  // s_best may still be read from a previous use
+  if (threadIdx.x < NSL * NK) s_best[threadIdx.x / NK][threadIdx.x % NK] = ~0ull;
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < NSL; ++s) win[s] = valid[s];
+#pragma unroll
+  for (int l = 0; l < NK; ++l) {
+#pragma unroll
+    for (int s = 0; s < NSL; ++s) {
+      const unsigned long long v = warp_min_u64(win[s] ? key[s][l] : ~0ull);
+      if ((threadIdx.x & 31) == 0 && v != ~0ull) atomicMin(&s_best[s][l], v);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < NSL; ++s) win[s] = win[s] && key[s][l] == s_best[s][l];
+  }
+}
+
+// Lexicographic keys (smaller is better) of a farthest-point candidate under
+// cand_better: larger d, then the chain's lex direction, then lower id; the
+// index makes the tuple unique.
+SH_DEV void cand_keys(const Cand& a, bool lower, unsigned long long (&key)[4]) {
+  const unsigned long long kx = fkey(a.x), ky = fkey(a.y);
+  key[0] = ~(unsigned long long)__double_as_longlong(a.d);
+  key[1] = lower ? kx : ~kx;
+  key[2] = lower ? ky : ~ky;
+  key[3] = ((unsigned long long)a.id << 32) | a.pos;
+}
+
 // full-warp argmax of one chain's candidates (all lanes end with the winner)
 SH_DEV Cand warp_best(Cand c, bool lower) {
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) {
     const Cand o = shfl_xor_cand(c, m);
-    if (cand_better(o, c, lower)) c = o;
+    if (cand_better_k(o, c, lower)) c = o;
   }
   return c;
 }

@@ -118,6 +118,19 @@ struct K1Partial {
   unsigned long long bad;
 };
 
+// farthest-point candidate (distance d of point (x, y), id, input index)
+struct Cand {
+  double d, x, y;
+  uint32_t id, pos;
+};
+
+// K2's per-CTA result, combined by every CTA of K3
+struct K2Partial {
+  Cand a[2];                // farthest candidate of the lower / upper chain
+  unsigned long long kept;  // points surviving the quadrilateral filter
+  uint32_t noncol, pad;     // some point off the line P0 -> Pr
+};
+
 // 64-byte route entry of an old segment s: head A, farthest point C, next
 // head B (hull.cpp:186-201 restated per segment).
 struct __align__(16) Route {
@@ -197,6 +210,8 @@ struct Bufs {
   Ctl* ctl;
   uint32_t* epoch;        // launch-epoch counter of the generator's look-back scan
   K1Partial* k1part;
+  K2Partial* k2part;
+  uint32_t k1_grid, k2_grid;  // CTAs of K1 / K2 (partials to combine)
   StatRec* stats;
   unsigned long long* tile_status;
   uint32_t* blk_cnt;      // [2 * MAX_ROUND_BLOCKS] per-CTA counts of a large table scan

@@ -45,78 +45,6 @@ SH_DEV bool nonfinite(double v) {
 // K1: extremes with directional ties (hull.cpp:25-45) + first non-finite index
 // ===========================================================================
 
-template <int DIR>
-SH_DEV bool ext_better(const ExtRec& a, const ExtRec& b) {
-  if (b.pos == NONE) return a.pos != NONE;
-  if (a.pos == NONE) return false;
-  if (DIR == 0) {  // left: min x, then min y
-    if (a.x != b.x) return a.x < b.x;
-    if (a.y != b.y) return a.y < b.y;
-  } else if (DIR == 1) {  // bottom: min y, then max x
-    if (a.y != b.y) return a.y < b.y;
-    if (a.x != b.x) return a.x > b.x;
-  } else if (DIR == 2) {  // right: max x, then max y
-    if (a.x != b.x) return a.x > b.x;
-    if (a.y != b.y) return a.y > b.y;
-  } else {  // top: max y, then min x
-    if (a.y != b.y) return a.y > b.y;
-    if (a.x != b.x) return a.x < b.x;
-  }
-  return a.id < b.id;  // exact duplicates: lowest index (strict compares)
-}
-
-SH_DEV ExtRec shfl_ext(const ExtRec& e, int m) {
-  ExtRec o;
-  o.x = __shfl_xor_sync(FULL, e.x, m);
-  o.y = __shfl_xor_sync(FULL, e.y, m);
-  o.id = __shfl_xor_sync(FULL, e.id, m);
-  o.pos = __shfl_xor_sync(FULL, e.pos, m);
-  return o;
-}
-
-SH_DEV void warp_reduce_ext(ExtRec* e, unsigned long long& bad) {
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) {
-    ExtRec o;
-    o = shfl_ext(e[0], m);
-    if (ext_better<0>(o, e[0])) e[0] = o;
-    o = shfl_ext(e[1], m);
-    if (ext_better<1>(o, e[1])) e[1] = o;
-    o = shfl_ext(e[2], m);
-    if (ext_better<2>(o, e[2])) e[2] = o;
-    o = shfl_ext(e[3], m);
-    if (ext_better<3>(o, e[3])) e[3] = o;
-    const unsigned long long ob = __shfl_xor_sync(FULL, bad, m);
-    bad = ob < bad ? ob : bad;
-  }
-}
-
-// reduce (e, bad) over the block; result valid in thread 0
-SH_DEV void block_reduce_ext(ExtRec* e, unsigned long long& bad) {
-  __shared__ ExtRec s_e[4][MAXW];
-  __shared__ unsigned long long s_bad[MAXW];
-  const int nw = blockDim.x >> 5;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  warp_reduce_ext(e, bad);
-  if (lane == 0) {
-    for (int k = 0; k < 4; ++k) s_e[k][warp] = e[k];
-    s_bad[warp] = bad;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    for (int k = 0; k < 4; ++k) {
-      if (lane < nw) {
-        e[k] = s_e[k][lane];
-      } else {
-        e[k].pos = NONE;
-      }
-    }
-    bad = lane < nw ? s_bad[lane] : ~0ull;
-    warp_reduce_ext(e, bad);
-  }
-  __syncthreads();
-}
-
 // One point, visited in increasing index order within a thread, so strict
 // comparisons keep the lowest index among exact duplicates (hull.cpp:39-43).
 // With caller ids (shard merge) the id decides exact duplicates explicitly.
@@ -141,32 +69,35 @@ SH_DEV void ext_visit(ExtRec (&e)[4], unsigned long long& bad, double x, double 
   }
 }
 
-// Thread 0, once the four extremes and the first bad index are known:
-// degenerate statuses (hull.cpp:222-237) and the quadrilateral (hull.cpp:58-74).
-SH_DEV void finalize_extremes(const Bufs& B, const ExtRec (&e)[4], unsigned long long bad) {
-  Ctl* c = B.ctl;
-  c->ticket = 0;
-  c->bad_index = bad;
-  // round-0 farthest slots (K2 offers into Slot[0]; hull_kernels.cuh)
-  rec_clear(&B.Sd[0][0], &B.Srec[0][0]);
-  rec_clear(&B.Sd[0][1], &B.Srec[0][1]);
-  c->mark[0] = globaltimer_ns() - c->t0_ns;
-  if (bad != ~0ull) {
-    c->status = ST_NONFINITE;
-    return;
-  }
+// The extremes' consequences (hull.cpp:222-237 statuses, hull.cpp:58-74
+// quadrilateral), computed from the four extremes and the first bad index.
+struct Fin {
+  uint32_t status;
+  int distinct, nedges;
+  unsigned long long bad;
+  ExtRec e[4];
+  double edges[4][4];  // (ax, ay, ex, ey)
+};
+
+SH_DEV void compute_fin(Fin& f, const ExtRec (&e)[4], unsigned long long bad) {
+  f.status = ST_RUNNING;
+  f.bad = bad;
+  f.distinct = 0;
+  f.nedges = 0;
   for (int k = 0; k < 4; ++k) {
-    c->ext_x[k] = e[k].x;
-    c->ext_y[k] = e[k].y;
-    c->ext_id[k] = e[k].id;
-    c->ext_pos[k] = e[k].pos;
+    f.e[k] = e[k];
+    for (int j = 0; j < 4; ++j) f.edges[k][j] = 0.0;
+  }
+  if (bad != ~0ull) {
+    f.status = ST_NONFINITE;
+    return;
   }
   if (e[0].x == e[2].x && e[0].y == e[2].y) {  // hull.cpp:234-237
-    c->status = ST_SINGLE;
+    f.status = ST_SINGLE;
     return;
   }
-  // hull.cpp:58-74: corners [left, bottom, right, top], distinct count and
-  // the edges between consecutive non-equal corners (with wrap-around)
+  // corners [left, bottom, right, top], distinct count and the edges between
+  // consecutive non-equal corners (with wrap-around)
   int distinct = 0;
   for (int a = 0; a < 4; ++a) {
     bool seen = false;
@@ -179,18 +110,77 @@ SH_DEV void finalize_extremes(const Bufs& B, const ExtRec (&e)[4], unsigned long
     const ExtRec& qq = e[(a + 1) & 3];
     if (!(p.x == qq.x && p.y == qq.y)) {
       const Edge ed = make_edge(p.x, p.y, qq.x, qq.y);
-      c->edges[ne][0] = ed.ax;
-      c->edges[ne][1] = ed.ay;
-      c->edges[ne][2] = ed.ex;
-      c->edges[ne][3] = ed.ey;
+      f.edges[ne][0] = ed.ax;
+      f.edges[ne][1] = ed.ay;
+      f.edges[ne][2] = ed.ex;
+      f.edges[ne][3] = ed.ey;
       ++ne;
     }
   }
-  for (int k = ne; k < 4; ++k)
-    for (int j = 0; j < 4; ++j) c->edges[k][j] = 0.0;
-  c->distinct = distinct;
-  c->nedges = ne;
+  f.distinct = distinct;
+  f.nedges = ne;
+}
+
+// one thread publishes Fin in the control block (later kernels, the host)
+SH_DEV void write_fin(Ctl* c, const Fin& f) {
+  c->bad_index = f.bad;
+  for (int k = 0; k < 4; ++k) {
+    c->ext_x[k] = f.e[k].x;
+    c->ext_y[k] = f.e[k].y;
+    c->ext_id[k] = f.e[k].id;
+    c->ext_pos[k] = f.e[k].pos;
+    for (int j = 0; j < 4; ++j) c->edges[k][j] = f.edges[k][j];
+  }
+  c->distinct = f.distinct;
+  c->nedges = f.nedges;
+  if (f.status != ST_RUNNING) c->status = f.status;
+}
+
+// Thread 0 of a single-CTA path: extremes -> control block.
+SH_DEV void finalize_extremes(const Bufs& B, const ExtRec (&e)[4], unsigned long long bad) {
+  Ctl* c = B.ctl;
+  Fin f;
+  compute_fin(f, e, bad);
+  write_fin(c, f);
   c->mark[0] = globaltimer_ns() - c->t0_ns;
+}
+
+// Lexicographic keys (smaller is better) of the four directional extremes
+// (hull.cpp:25-45): left = min x, min y; bottom = min y, max x; right = max x,
+// max y; top = max y, min x; then the id (caller id or index), then the index.
+SH_DEV void ext_keys(const ExtRec (&e)[4], unsigned long long (&key)[4][3], bool (&valid)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const unsigned long long kx = fkey(e[k].x), ky = fkey(e[k].y);
+    key[k][0] = k == 0 ? kx : k == 1 ? ky : k == 2 ? ~kx : ~ky;
+    key[k][1] = k == 0 ? ky : k == 1 ? ~kx : k == 2 ? ~ky : kx;
+    key[k][2] = ((unsigned long long)e[k].id << 32) | e[k].pos;
+    valid[k] = e[k].pos != NONE;
+  }
+}
+
+// CTA-wide extremes + first bad index of the records the threads hold; the
+// winners are copied to out[] (shared or global), a direction without any
+// record gets pos = NONE.  Contains barriers.
+SH_DEV void cta_extremes(const ExtRec (&e)[4], unsigned long long bad, ExtRec* out,
+                         unsigned long long* out_bad) {
+  __shared__ unsigned long long s_best[4][3];
+  __shared__ unsigned long long s_bad;
+  unsigned long long key[4][3];
+  bool valid[4], win[4];
+  ext_keys(e, key, valid);
+  if (threadIdx.x == 0) s_bad = ~0ull;
+  cta_lexmin<4, 3>(key, valid, s_best, win);  // starts with a barrier
+  if (bad != ~0ull) atomicMin(&s_bad, bad);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (win[k]) out[k] = e[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 4; ++k)
+      if (s_best[k][0] == ~0ull) out[k].pos = NONE;
+    *out_bad = s_bad;
+  }
 }
 
 template <bool IDS>
@@ -281,44 +271,11 @@ __global__ void __launch_bounds__(Cfg1::TPB, 1) k1_extremes(Bufs B) {
       if (e[3].pos != NONE) atomicMax(&s_thr[3], okey(e[3].y));
     }
   });
+  if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[blockIdx.x] = globaltimer_ns() - c->t0_ns;
 
-  block_reduce_ext(e, bad);
-  __shared__ int s_last;
-  if (threadIdx.x == 0) {
-    K1Partial pt;
-    for (int k = 0; k < 4; ++k) pt.e[k] = e[k];
-    pt.bad = bad;
-    B.k1part[blockIdx.x] = pt;
-    __threadfence();
-    s_last = atomicAdd(&c->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
-  // last CTA: combine the per-CTA partials
-  for (int k = 0; k < 4; ++k) e[k].pos = NONE;
-  bad = ~0ull;
-  for (uint32_t p = threadIdx.x; p < gridDim.x; p += blockDim.x) {
-    const K1Partial* qp = B.k1part + p;
-    ExtRec o[4];
-    for (int k = 0; k < 4; ++k) {
-      o[k].x = __ldcg(&qp->e[k].x);
-      o[k].y = __ldcg(&qp->e[k].y);
-      o[k].id = __ldcg(&qp->e[k].id);
-      o[k].pos = __ldcg(&qp->e[k].pos);
-    }
-    if (ext_better<0>(o[0], e[0])) e[0] = o[0];
-    if (ext_better<1>(o[1], e[1])) e[1] = o[1];
-    if (ext_better<2>(o[2], e[2])) e[2] = o[2];
-    if (ext_better<3>(o[3], e[3])) e[3] = o[3];
-    const unsigned long long ob = __ldcg(&qp->bad);
-    bad = ob < bad ? ob : bad;
-  }
-  block_reduce_ext(e, bad);
-  if (threadIdx.x != 0) return;
-
-  finalize_extremes(B, e, bad);
+  // this CTA's extremes -> its partial (the next kernel combines them)
+  K1Partial* part = B.k1part + blockIdx.x;
+  cta_extremes(e, bad, part->e, &part->bad);
 }
 
 // ===========================================================================
@@ -340,28 +297,63 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   TileRing<Cfg2::T, Cfg2::NS, IDS, 0, Cfg2::CW> R;
   R.carve(smem_raw);
   Ctl* c = B.ctl;
-  pdl_wait();               // K1's extremes are complete and visible
+  pdl_wait();               // K1's partial extremes are complete and visible
   pdl_launch_dependents();  // K3 may be scheduled on SMs this kernel frees
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) c->mark[1] = globaltimer_ns() - c->t0_ns;
+  // ---- every CTA combines K1's per-CTA extremes (no serial last-CTA step) ----
+  __shared__ Fin s_fin;
+  {
+    ExtRec e[4];
+    unsigned long long bad = ~0ull;
+    for (int k = 0; k < 4; ++k) e[k].id = e[k].pos = NONE;
+    if (threadIdx.x < B.k1_grid) {
+      const K1Partial* qp = B.k1part + threadIdx.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        e[k].x = __ldcg(&qp->e[k].x);
+        e[k].y = __ldcg(&qp->e[k].y);
+        e[k].id = __ldcg(&qp->e[k].id);
+        e[k].pos = __ldcg(&qp->e[k].pos);
+      }
+      bad = __ldcg(&qp->bad);
+    }
+    __shared__ ExtRec s_ext[4];
+    __shared__ unsigned long long s_bad;
+    cta_extremes(e, bad, s_ext, &s_bad);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const ExtRec ee[4] = {s_ext[0], s_ext[1], s_ext[2], s_ext[3]};
+      compute_fin(s_fin, ee, s_bad);
+      if (blockIdx.x == 0) {
+        write_fin(c, s_fin);
+        const unsigned long long now = globaltimer_ns() - c->t0_ns;
+        c->mark[0] = now;
+        c->mark[1] = now;
+        // round 1 (K3) offers its farthest points into Slot[1] (<= 4 segments)
+        for (int t = 0; t < 4; ++t) rec_clear(&B.Sd[1][t], &B.Srec[1][t]);
+      }
+    }
+    __syncthreads();
+  }
+  if (s_fin.status != ST_RUNNING) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n = B.n;
   const double* __restrict__ X = B.in_x;
   const double* __restrict__ Y = B.in_y;
   const uint32_t* __restrict__ I = B.in_id;
-  const uint32_t p0 = c->ext_pos[0], pr = c->ext_pos[2];
-  const double x0 = c->ext_x[0], y0 = c->ext_y[0], xr = c->ext_x[2], yr = c->ext_y[2];
+  const uint32_t p0 = s_fin.e[0].pos, pr = s_fin.e[2].pos;
+  const double x0 = s_fin.e[0].x, y0 = s_fin.e[0].y, xr = s_fin.e[2].x, yr = s_fin.e[2].y;
   const Edge E01 = make_edge(x0, y0, xr, yr);  // lower chain base line P0 -> Pr
   const Edge E10 = make_edge(xr, yr, x0, y0);  // upper chain base line Pr -> P0 (wrap)
-  const bool filt = FILTER && c->distinct >= 3;
-  const int ne = filt ? c->nedges : 0;
+  const bool filt = FILTER && s_fin.distinct >= 3;
+  const int ne = filt ? s_fin.nedges : 0;
   Edge Q[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    Q[k].ax = c->edges[k][0];
-    Q[k].ay = c->edges[k][1];
-    Q[k].ex = c->edges[k][2];
-    Q[k].ey = c->edges[k][3];
+    Q[k].ax = s_fin.edges[k][0];
+    Q[k].ay = s_fin.edges[k][1];
+    Q[k].ex = s_fin.edges[k][2];
+    Q[k].ey = s_fin.edges[k][3];
   }
   Cand a0 = empty_cand(), a1 = empty_cand();
   uint32_t kept = 0;
@@ -380,9 +372,9 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   // top) and the chain base lines start at left (P0) and right (Pr), so the
   // per-point differences p - corner are shared by the 6 cross products:
   // the same RN operations as cross() (geometry.hpp:17-19), computed once.
-  const bool quad4 = filt && ne == 4 && c->distinct == 4;
-  const double cxL = c->ext_x[0], cyL = c->ext_y[0], cxB = c->ext_x[1], cyB = c->ext_y[1];
-  const double cxR = c->ext_x[2], cyR = c->ext_y[2], cxT = c->ext_x[3], cyT = c->ext_y[3];
+  const bool quad4 = filt && ne == 4 && s_fin.distinct == 4;
+  const double cxL = s_fin.e[0].x, cyL = s_fin.e[0].y, cxB = s_fin.e[1].x, cyB = s_fin.e[1].y;
+  const double cxR = s_fin.e[2].x, cyR = s_fin.e[2].y, cxT = s_fin.e[3].x, cyT = s_fin.e[3].y;
   auto xprod = [](double ex, double ey, double dx, double dy) {
     return __dsub_rn(__dmul_rn(ex, dy), __dmul_rn(ey, dx));
   };
@@ -522,68 +514,43 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
     pass(std::integral_constant<int, 2>{});
   else
     pass(std::integral_constant<int, 0>{});
+  if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[256 + blockIdx.x] = globaltimer_ns() - c->t0_ns;
 
-  // block reduction of the two chains' farthest candidates
-  __shared__ Cand s_a[2][MAXW];
-  __shared__ uint32_t s_kept[MAXW];
-  const int nwb = blockDim.x >> 5;
-  __shared__ int s_last;
-  a0 = warp_best(a0, true);
-  a1 = warp_best(a1, false);
-  const bool nc_any = __any_sync(FULL, noncol);
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) kept += __shfl_xor_sync(FULL, kept, m);
-  if (lane == 0) {
-    s_a[0][warp] = a0;
-    s_a[1][warp] = a1;
-    s_kept[warp] = kept | (nc_any ? 0x80000000u : 0u);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    a0 = lane < nwb ? s_a[0][lane] : empty_cand();
-    a1 = lane < nwb ? s_a[1][lane] : empty_cand();
-    a0 = warp_best(a0, true);
-    a1 = warp_best(a1, false);
+  // this CTA's farthest candidates of both chains, kept count and
+  // collinearity -> its partial (K3 combines the partials)
+  {
+    __shared__ unsigned long long s_best2[2][4];
+    __shared__ unsigned long long s_kb;
+    __shared__ uint32_t s_nc;
+    unsigned long long key[2][4];
+    bool valid[2], win[2];
+    cand_keys(a0, true, key[0]);
+    cand_keys(a1, false, key[1]);
+    valid[0] = a0.d > 0.0;
+    valid[1] = a1.d > 0.0;
+    if (threadIdx.x == 0) {
+      s_kb = 0;
+      s_nc = 0;
+    }
+    cta_lexmin<2, 4>(key, valid, s_best2, win);  // starts with a barrier
+    const uint32_t wk = __reduce_add_sync(FULL, kept);
+    const bool wnc = __any_sync(FULL, noncol);
     if (lane == 0) {
-      unsigned long long kb = 0;
-      bool nc = false;
-      for (int w = 0; w < nwb; ++w) {
-        kb += s_kept[w] & 0x7FFFFFFFu;
-        nc = nc || (s_kept[w] >> 31);
-      }
-      if (kb) atomicAdd(&c->kept, kb);
-      if (nc) atomicOr(&c->noncollinear, 1u);
-      if (a0.d > 0.0) rec_offer(&B.Sd[0][0], &B.Srec[0][0], a0, true);
-      if (a1.d > 0.0) rec_offer(&B.Sd[0][1], &B.Srec[0][1], a1, false);
-      __threadfence();
-      s_last = atomicAdd(&c->ticket, 1u) == gridDim.x - 1;
+      if (wk) atomicAdd(&s_kb, (unsigned long long)wk);
+      if (wnc) s_nc = 1u;
+    }
+    K2Partial* part = B.k2part + blockIdx.x;
+    if (win[0]) part->a[0] = a0;
+    if (win[1]) part->a[1] = a1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_best2[0][0] == ~0ull) part->a[0] = empty_cand();
+      if (s_best2[1][0] == ~0ull) part->a[1] = empty_cand();
+      part->kept = s_kb;
+      part->noncol = s_nc;
+      if (blockIdx.x == 0) c->mark[2] = globaltimer_ns() - c->t0_ns;
     }
   }
-  __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
-  __threadfence();
-  c->ticket = 0;
-  // round-1 farthest slots (round 1 offers into Slot[1]; its table has <= 4 entries)
-  for (int t = 0; t < 4; ++t) rec_clear(&B.Sd[1][t], &B.Srec[1][t]);
-  if (!*(volatile uint32_t*)&c->noncollinear) {
-    c->status = ST_COLLINEAR;  // hull.cpp:238-248
-  } else {
-    // first split (hull.cpp:101-158): P0 heads the lower chain, Pr the upper
-    B.Tx[0][0] = x0;
-    B.Ty[0][0] = y0;
-    B.Tid[0][0] = c->ext_id[0];
-    B.Tx[0][1] = xr;
-    B.Ty[0][1] = yr;
-    B.Tid[0][1] = c->ext_id[2];
-    const unsigned long long kept_all = *(volatile unsigned long long*)&c->kept;
-    c->S_cur = 2;
-    c->Slo_cur = 1;
-    c->m_cur = (uint32_t)(kept_all - 2);
-    c->round = 0;
-    if (kept_all == 2) c->status = ST_DONE;
-  }
-  c->mark[2] = globaltimer_ns() - c->t0_ns;
-  __threadfence();
 }
 
 // ===========================================================================
@@ -614,9 +581,17 @@ __global__ void __launch_bounds__(1024, 1) k_small_pre(Bufs B) {
   unsigned long long bad = ~0ull;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
     ext_visit<IDS>(e, bad, __ldg(X + i), __ldg(Y + i), IDS ? __ldg(I + i) : i, i);
-  block_reduce_ext(e, bad);
-  if (threadIdx.x == 0) finalize_extremes(B, e, bad);
-  __syncthreads();
+  {
+    __shared__ ExtRec s_ext[4];
+    __shared__ unsigned long long s_bad;
+    cta_extremes(e, bad, s_ext, &s_bad);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const ExtRec ee[4] = {s_ext[0], s_ext[1], s_ext[2], s_ext[3]};
+      finalize_extremes(B, ee, s_bad);
+    }
+    __syncthreads();
+  }
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
 
   // ---- filter + classes + round-0 farthest + dense member list (K2) ----

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   __shared__ uint32_t s_ws[MAXW + 1];
   __shared__ int s_last;
   Ctl* c = B.ctl;
-  pdl_wait();               // K2's classes and farthest records are complete and visible
+  pdl_wait();               // K2's classes and partials are complete and visible
   pdl_launch_dependents();  // the round kernel may be scheduled on SMs this kernel frees
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -223,23 +223,97 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   const double* __restrict__ Y = B.in_y;
   const uint32_t* __restrict__ I = B.in_id;
 
+  // ---- every CTA combines K2's per-CTA partials (hull.cpp:101-158): the
+  // farthest point of each chain, the kept count and collinearity ----
+  __shared__ Cand s_cand[2];
+  __shared__ unsigned long long s_best2[2][4];
+  __shared__ unsigned long long s_kept;
+  __shared__ uint32_t s_nc, s_status;
+  {
+    Cand a[2] = {empty_cand(), empty_cand()};
+    unsigned long long kb = 0;
+    uint32_t nc = 0;
+    if (threadIdx.x < B.k2_grid) {
+      const K2Partial* qp = B.k2part + threadIdx.x;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        a[ch].d = __ldcg(&qp->a[ch].d);
+        a[ch].x = __ldcg(&qp->a[ch].x);
+        a[ch].y = __ldcg(&qp->a[ch].y);
+        a[ch].id = __ldcg(&qp->a[ch].id);
+        a[ch].pos = __ldcg(&qp->a[ch].pos);
+      }
+      kb = __ldcg(&qp->kept);
+      nc = __ldcg(&qp->noncol);
+    }
+    unsigned long long key[2][4];
+    bool valid[2], win[2];
+    cand_keys(a[0], true, key[0]);
+    cand_keys(a[1], false, key[1]);
+    valid[0] = a[0].d > 0.0;
+    valid[1] = a[1].d > 0.0;
+    if (threadIdx.x == 0) {
+      s_kept = 0;
+      s_nc = 0;
+    }
+    cta_lexmin<2, 4>(key, valid, s_best2, win);  // starts with a barrier
+    if (kb) atomicAdd(&s_kept, kb);
+    if (nc) s_nc = 1u;
+    if (win[0]) s_cand[0] = a[0];
+    if (win[1]) s_cand[1] = a[1];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int ch = 0; ch < 2; ++ch)
+        if (s_best2[ch][0] == ~0ull) s_cand[ch] = empty_cand();
+      const unsigned long long kept_all = s_kept;
+      const uint32_t st = !s_nc ? ST_COLLINEAR : kept_all == 2 ? ST_DONE : ST_RUNNING;
+      s_status = st;
+      if (blockIdx.x == 0) {
+        const unsigned long long now = globaltimer_ns() - c->t0_ns;
+        c->mark[2] = now;
+        c->mark[3] = now;
+        c->kept = kept_all;
+        c->noncollinear = s_nc;
+        if (st == ST_COLLINEAR) {
+          c->status = ST_COLLINEAR;  // hull.cpp:238-248
+        } else {
+          // first split (hull.cpp:101-158): P0 heads the lower chain, Pr the upper
+          B.Tx[0][0] = c->ext_x[0];
+          B.Ty[0][0] = c->ext_y[0];
+          B.Tid[0][0] = c->ext_id[0];
+          B.Tx[0][1] = c->ext_x[2];
+          B.Ty[0][1] = c->ext_y[2];
+          B.Tid[0][1] = c->ext_id[2];
+          c->S_cur = 2;
+          c->Slo_cur = 1;
+          c->m_cur = (uint32_t)(kept_all - 2);
+          c->round = 0;
+          if (st == ST_DONE) c->status = ST_DONE;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_status != ST_RUNNING) return;
+  }
+
   // ---- table phase (S = 2: the lower chain P0->Pr and the upper chain Pr->P0) ----
   if (threadIdx.x == 0) {
-    if (blockIdx.x == 0) c->mark[3] = globaltimer_ns() - c->t0_ns;
     R.init();
     uint32_t ns = 0, Slon = 1;
+    const double hx[2] = {__ldcg(&c->ext_x[0]), __ldcg(&c->ext_x[2])};
+    const double hy[2] = {__ldcg(&c->ext_y[0]), __ldcg(&c->ext_y[2])};
+    const uint32_t hid[2] = {__ldcg(&c->ext_id[0]), __ldcg(&c->ext_id[2])};
     for (int s = 0; s < 2; ++s) {
-      const SlotRec* cr = B.Srec[0] + s;
-      const uint32_t cid = __ldcg(&cr->id);
-      const bool split = cid != NONE;
+      const Cand& cr = s_cand[s];
+      const bool split = cr.d > 0.0;
       Route r;
-      r.ax = __ldcg(B.Tx[0] + s);
-      r.ay = __ldcg(B.Ty[0] + s);
-      r.bx = __ldcg(B.Tx[0] + (s ^ 1));
-      r.by = __ldcg(B.Ty[0] + (s ^ 1));
-      r.cx = split ? __ldcg(&cr->x) : 0.0;
-      r.cy = split ? __ldcg(&cr->y) : 0.0;
-      r.cid = cid;
+      r.ax = hx[s];
+      r.ay = hy[s];
+      r.bx = hx[s ^ 1];
+      r.by = hy[s ^ 1];
+      r.cx = split ? cr.x : 0.0;
+      r.cy = split ? cr.y : 0.0;
+      r.cid = split ? cr.id : NONE;
       r.ns = ns;
       r.flags = (split ? RT_SPLIT : 0u) | (s == 0 ? RT_LOWER : 0u);
       r.pad = 0;
@@ -247,7 +321,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
       if (blockIdx.x == 0) {
         B.Tx[1][ns] = r.ax;
         B.Ty[1][ns] = r.ay;
-        B.Tid[1][ns] = __ldcg(B.Tid[0] + s);
+        B.Tid[1][ns] = hid[s];
         if (split) {
           B.Tx[1][ns + 1] = r.cx;
           B.Ty[1][ns + 1] = r.cy;
@@ -346,6 +420,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
     else
       tile(std::false_type{}, s, first, cnt);
   });
+  if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[512 + blockIdx.x] = globaltimer_ns() - c->t0_ns;
 
   // ---- flush the CTA's records to the global slots of round 2's argmax ----
   __syncthreads();

@@ -152,6 +152,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   const size_t o_ctl = take(HOST_RES_STATS + sizeof(StatRec) * STATS_CAP);  // Ctl, then the stats
   const size_t o_epoch = take(sizeof(uint32_t));
   const size_t o_k1 = take(sizeof(K1Partial) * ws->stream_grid);
+  const size_t o_k2 = take(sizeof(K2Partial) * ws->stream_grid);
   const size_t o_blk = take(sizeof(uint32_t) * 2 * MAX_ROUND_BLOCKS);
   const size_t o_dbg = take(sizeof(unsigned long long) * MAX_ROUND_BLOCKS);
   const size_t o_tiles = take(sizeof(unsigned long long) * ws->tiles_cap);
@@ -187,6 +188,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   const uint32_t one = 1;
   CK(cudaMemcpy(ws->epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
   B.k1part = (K1Partial*)(a + o_k1);
+  B.k2part = (K2Partial*)(a + o_k2);
   B.stats = (StatRec*)(a + o_ctl + HOST_RES_STATS);
   B.blk_cnt = (uint32_t*)(a + o_blk);
   B.dbg = (unsigned long long*)(a + o_dbg);
@@ -334,6 +336,8 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
     return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + T - 1) / T, (uint64_t)ws.stream_grid));
   };
   const int g1 = grid_of(Cfg1::T), g2 = grid_of(Cfg2::T), gs = grid_of(Cfg3::T);
+  B.k1_grid = (uint32_t)g1;
+  B.k2_grid = (uint32_t)g2;
   // K3's CTA j owns run j of the live set: its tiles j, j + gs, ...
   const uint64_t ntiles3 = (n + Cfg3::T - 1) / Cfg3::T;
   B.run_q = (uint32_t)((ntiles3 + gs - 1) / gs * Cfg3::T);

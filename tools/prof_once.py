@@ -43,6 +43,16 @@ for _ in range(reps):
             print(f"   trace round {trace} (us since K1 start: start, table, prefix, points, flush, barrier, [winner]):", [round(t, 2) for t in ts])
         cb = (ctypes.c_ulonglong * 1024)()
         L.sh_b200_debug_last_ctas(cb, 1024)
+        if trace == 255:
+            import statistics
+            for name, off in (("K1", 0), ("K2", 256), ("K3", 512)):
+                e = sorted(cb[off + i] / 1e3 for i in range(148) if cb[off + i])
+                if e:
+                    print(f"   {name} CTA stream ends: min {e[0]:.1f} median {statistics.median(e):.1f} "
+                          f"p90 {e[int(len(e) * 0.9)]:.1f} max {e[-1]:.1f} us", flush=True)
+            print("   K1 last CTA (us): ticket won, fence, combined, reduced, finalized:",
+                  [round(cb[768 + k] / 1e3, 1) for k in range(8)], flush=True)
+            continue
         ends = sorted(cb[i] / 1e3 for i in range(1024) if cb[i])
         slow = sorted((cb[i] / 1e3, i) for i in range(1024) if cb[i])[-10:]
         print("   slowest CTAs (end us, cta):", [(round(t, 1), i) for t, i in slow])
