@@ -58,13 +58,13 @@ struct StreamCfg {
 #define SHB_K1_NS 4
 #endif
 #ifndef SHB_K2_TPB
-#define SHB_K2_TPB 512
+#define SHB_K2_TPB 768
 #endif
 #ifndef SHB_K2_CH
 #define SHB_K2_CH 2
 #endif
 #ifndef SHB_K2_NS
-#define SHB_K2_NS 4
+#define SHB_K2_NS 3
 #endif
 #ifndef SHB_K3_TPB
 #define SHB_K3_TPB 1024

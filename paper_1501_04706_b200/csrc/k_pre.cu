@@ -441,7 +441,10 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
       const double dxL = __dsub_rn(x, cxL), dyL = __dsub_rn(y, cyL);
       const double dxR = __dsub_rn(x, cxR), dyR = __dsub_rn(y, cyR);
       cl[q] = xprod(E01.ex, E01.ey, dxL, dyL);         // cross(P0, Pr, p)
-      du[q] = -xprod(E10.ex, E10.ey, dxR, dyR);        // outward_distance(Pr, P0, p)
+      // outward_distance(Pr, P0, p) = -cross: RN is symmetric, so swapping the
+      // products gives the same value (up to the sign of a zero, which the
+      // d > 0 tests ignore) without the extra negation
+      du[q] = __dsub_rn(__dmul_rn(E10.ey, dxR), __dmul_rn(E10.ex, dyR));
       bool inside = false;
       if (QK == 1) {  // hull.cpp:80-90: discard iff cross > 0 for every edge
         const double dxB = __dsub_rn(x, cxB), dyB = __dsub_rn(y, cyB);
