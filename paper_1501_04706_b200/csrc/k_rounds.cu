@@ -929,6 +929,10 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, bool recs_s
 }
 
 constexpr uint32_t ROUND_TARGET = 4 * RCTHREADS;  // live points per active CTA before CTAs retire
+#ifndef SHB_ONE_CTA_WORK
+#define SHB_ONE_CTA_WORK 0
+#endif
+constexpr uint32_t ONE_CTA_WORK = SHB_ONE_CTA_WORK;
 
 __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -971,7 +975,9 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     // same m, so the decision is consistent
     {
       const uint32_t work = max(m, S);  // live points, or segments of a large table
-      const uint32_t want = max(1u, min(P, (work + target - 1) / target));
+      // below ONE_CTA_WORK a lone CTA beats a grid: no slot flush, no barrier
+      const uint32_t want =
+          work <= ONE_CTA_WORK ? 1u : max(1u, min(P, (work + target - 1) / target));
       if (blockIdx.x >= want) return;
       P = want;
     }
@@ -1099,14 +1105,18 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
           __syncwarp();
           if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.lebar[st]);  // stage read
         } else {
-          uint32_t rb = 0;
-          {
+          // each point finds its run by binary search over the run prefix
+          // (the positions of a tile can span dozens of short runs)
+          uint32_t phys[KR_U];
+#pragma unroll
+          for (int u = 0; u < KR_U; ++u) {
+            const uint32_t v0 = t0 + u * RCTHREADS + threadIdx.x;
             uint32_t a0 = 0, a1 = nruns;
             while (a1 - a0 > 1) {
               const uint32_t mid = (a0 + a1) >> 1;
-              if (s_pref[mid] <= t0) a0 = mid; else a1 = mid;
+              if (s_pref[mid] <= v0) a0 = mid; else a1 = mid;
             }
-            rb = a0;
+            phys[u] = a0 * q + (v0 - s_pref[a0]);
           }
 #pragma unroll
           for (int u = 0; u < KR_U; ++u) {
@@ -1115,12 +1125,8 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
             pid[u] = 0;
             oseg[u] = NONE;
             if (e < tc) {
-              const uint32_t v0 = t0 + e;
-              uint32_t b2 = rb;
-              while (v0 >= s_pref[b2 + 1]) ++b2;
-              const uint32_t phys = b2 * q + (v0 - s_pref[b2]);
-              const double2 v = __ldcg(Ixy + phys);
-              const uint2 is = __ldcg(Iis + phys);
+              const double2 v = __ldcg(Ixy + phys[u]);
+              const uint2 is = __ldcg(Iis + phys[u]);
               px[u] = v.x;
               py[u] = v.y;
               pid[u] = is.x;
