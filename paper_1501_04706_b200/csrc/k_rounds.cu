@@ -929,6 +929,9 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, bool recs_s
 }
 
 constexpr uint32_t ROUND_TARGET = 4 * RCTHREADS;  // live points per active CTA before CTAs retire
+#ifndef SHB_KR_REVERSE
+#define SHB_KR_REVERSE 1
+#endif
 #ifndef SHB_ONE_CTA_WORK
 #define SHB_ONE_CTA_WORK 0
 #endif
@@ -1044,6 +1047,9 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     const uint32_t lo = 2u * (uint32_t)((unsigned long long)(Mp / 2) * blockIdx.x / P);
     const uint32_t hi = 2u * (uint32_t)((unsigned long long)(Mp / 2) * (blockIdx.x + 1) / P);
     const uint32_t ntl = (hi - lo + LIVE_T - 1) / LIVE_T;
+    // tiles newest-first: the tail of each run was written last (by this
+    // round's predecessor) and is the part most likely still in L2
+    auto tile_at = [&](uint32_t k) { return SHB_KR_REVERSE ? ntl - 1 - k : k; };
     // ring stages/phases continue across rounds: tile kk of this round is
     // the CTA's (kbase + kk)-th tile overall.  Fragmented live sets (short
     // runs: many tiny bulk copies, each ~70 ns to issue) are read with plain
@@ -1051,7 +1057,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     const bool use_tma = Mp >= 256u * nruns;
     auto issue = [&](uint32_t kk) {  // producer lane
       const int st = (int)((kbase + kk) % LIVE_NS);
-      const uint32_t t0 = lo + kk * LIVE_T, t1 = min(hi, t0 + LIVE_T);
+      const uint32_t t0 = lo + tile_at(kk) * LIVE_T, t1 = min(hi, t0 + LIVE_T);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&sm.lbar[st], (t1 - t0) * 24u);
       uint32_t a0 = 0, a1 = nruns;
@@ -1081,7 +1087,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       for (uint32_t k = 0; k < ntl; ++k) {
         const int st = (int)((kbase + k) % LIVE_NS);
         const uint32_t ph = ((kbase + k) / LIVE_NS) & 1u;
-        const uint32_t t0 = lo + k * LIVE_T, tc = min(hi, t0 + LIVE_T) - t0;
+        const uint32_t t0 = lo + tile_at(k) * LIVE_T, tc = min(hi, t0 + LIVE_T) - t0;
         double px[KR_U], py[KR_U], pd[KR_U];
         uint32_t pid[KR_U], pseg[KR_U], oseg[KR_U];
         uint32_t keepm = 0, lowm = 0;
