@@ -281,7 +281,13 @@ def run_b200(a):
     from paper_1501_04706_b200 import _lib, dataio, hull
 
     world, rank, local = dist_env()
-    if world > 1:
+    # SHB_BENCH_SHARE_GPU=1 (test only): every rank on cuda:0 and the gather
+    # over gloo through host tensors, to exercise the N-rank path on one GPU
+    share = world > 1 and os.environ.get("SHB_BENCH_SHARE_GPU") == "1"
+    if share:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    elif world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -312,7 +318,7 @@ def run_b200(a):
            torch.empty(cap, dtype=torch.int64, device=dev))
     launches = [0]
 
-    from paper_1501_04706_b200 import shard
+    from paper_1501_04706_b200 import shard as shardmod
 
     def merge(dh):
         """all-gather the shard hulls (NCCL over NVLink) and hull them on every rank."""
@@ -320,7 +326,20 @@ def run_b200(a):
             m = hull.run_device(mx, my, a.mode, ids=mids, stream=sp, stats=False)
             launches[0] += m.kernel_launches
             return m
-        return shard.merged_hull(dh, first, world, dist.all_gather_into_tensor, hull_with_ids)
+        return shardmod.merged_hull(dh, first, world, all_gather, hull_with_ids)
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if share else dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_gather(out, inp):
+        if not share:
+            return dist.all_gather_into_tensor(out, inp)
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu())
+        out.copy_(o)
 
     def step(timings=False):
         dh = hull.run_device(x, y, a.mode, stream=sp, timings=timings, out=out)
@@ -354,10 +373,7 @@ def run_b200(a):
     clocks.stop()
     gpu_launches = launches[0]
     t_rank = sum(s.elapsed_time(e) for s, e in ev) / 1e3  # seconds over K steps
-    t_all = torch.tensor([t_rank], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
-    t_max = float(t_all.item())
+    t_max = max_over_ranks(t_rank)
     ms_per_step = t_max / a.steps * 1e3
     value = n_total / (t_max / a.steps) / 1e6
 
@@ -432,10 +448,7 @@ def run_b200(a):
             h_e, _ = e2e_step()
         t1.record(stream)
         barrier()
-        te = torch.tensor([t0.elapsed_time(t1) / 1e3], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        te = float(te.item()) / ke
+        te = max_over_ranks(t0.elapsed_time(t1) / 1e3) / ke
         e2e = {"value": n_total / te / 1e6, "unit": "Mpoints/s",
                "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": 16 * n_total,
