@@ -236,6 +236,9 @@ struct Bufs {
   // CTA run, the survivors that reached their segment's running maximum
   uint32_t* Wn[3];
   LiveCand* Lc;
+  // small tables, multi-CTA rounds: each CTA's farthest records, one row of
+  // NSLOT per CTA (ping-pong by round parity); Wn then names the winning row
+  SlotRec* Rc[2];
   Route* route;
 };
 // The control block and the round stats are contiguous in the arena, so ONE

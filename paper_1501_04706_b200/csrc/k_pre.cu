@@ -696,7 +696,10 @@ __global__ void __launch_bounds__(1024, 1) k_small_pre(Bufs B) {
       B.Srec[0][t].id = ab[t]->id;
     }
   }
-  for (int t = 0; t < 4; ++t) rec_clear(&B.Sd[1][t], &B.Srec[1][t]);
+  for (int t = 0; t < 4; ++t) {
+    rec_clear(&B.Sd[1][t], &B.Srec[1][t]);
+    B.Wn[1][t] = NONE;  // round 1 runs in the round kernel
+  }
   if (!nc) {
     c->status = ST_COLLINEAR;  // hull.cpp:238-248
   } else {

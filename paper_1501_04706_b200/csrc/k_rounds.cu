@@ -179,6 +179,49 @@ SH_DEV void flush_slots(const unsigned long long* s_db, const SlotRec* s_rec, ui
   }
 }
 
+// Lock-free flush of a multi-CTA round's small-table records: the CTA's
+// records go to its own row (plain stores), their distance bits to the
+// global running maxima (fire-and-forget atomicMax).  After the grid barrier,
+// claim_slots lets the rows that reached a slot's final maximum claim it.
+SH_DEV void flush_rows(const unsigned long long* s_db, const SlotRec* s_rec, uint32_t Sn,
+                       unsigned long long* Sd, SlotRec* row) {
+  for (uint32_t t = threadIdx.x; t < Sn; t += blockDim.x) {
+    const volatile SlotRec* r = s_rec + t;
+    SlotRec o;
+    o.d = r->d;
+    o.x = r->x;
+    o.y = r->y;
+    o.id = r->id;
+    o.lock = 0u;
+    row[t] = o;
+    if (o.id != NONE) atomicMax(Sd + t, (unsigned long long)__double_as_longlong(o.d));
+  }
+}
+
+// The CTA's records whose distance equals the slot's final maximum claim the
+// slot's winner word (this CTA's row index); exact ties run the full
+// comparator (hull.cpp:171-179) in a compare-and-swap loop over rows.
+SH_DEV void claim_slots(const SlotRec* s_rec, uint32_t Sn, uint32_t Slon,
+                        const unsigned long long* Sd, uint32_t* Wn, const SlotRec* rows) {
+  for (uint32_t t = threadIdx.x; t < Sn; t += blockDim.x) {
+    const volatile SlotRec* r = s_rec + t;
+    if (r->id == NONE) continue;
+    Cand me;
+    me.d = r->d; me.x = r->x; me.y = r->y; me.id = r->id; me.pos = 0;
+    if ((unsigned long long)__double_as_longlong(me.d) != __ldcg(Sd + t)) continue;
+    uint32_t cur = atomicCAS(Wn + t, NONE, blockIdx.x);
+    while (cur != NONE) {
+      const SlotRec* q = rows + (size_t)cur * NSLOT + t;
+      Cand o;
+      o.d = __ldcg(&q->d); o.x = __ldcg(&q->x); o.y = __ldcg(&q->y); o.id = __ldcg(&q->id); o.pos = 0;
+      if (!cand_better(me, o, t < Slon)) break;
+      const uint32_t prev = atomicCAS(Wn + t, cur, blockIdx.x);
+      if (prev == cur) break;
+      cur = prev;
+    }
+  }
+}
+
 // sum of nruns run counts, computed by the whole CTA (contains barriers)
 SH_DEV uint32_t sum_runs(const uint32_t* cnt, uint32_t nruns, uint32_t* s_ws) {
   uint32_t v = 0;
@@ -336,7 +379,10 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
     s_off = 0;
     for (int t = 0; t < 4; ++t) rec_clear(&s_db[t], &s_rec[t]);
     if (blockIdx.x == 0)  // clear round 2's slots
-      for (int t = 0; t < 8; ++t) rec_clear(&B.Sd[2][t], &B.Srec[2][t]);
+      for (int t = 0; t < 8; ++t) {
+        rec_clear(&B.Sd[2][t], &B.Srec[2][t]);
+        B.Wn[2][t] = NONE;
+      }
   }
   __syncthreads();
   const uint32_t Sn = s_Sn, Slon = s_Slon;
@@ -428,7 +474,12 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
     Oxy[run_base + s_off] = make_double2(0.0, 0.0);
     Ois[run_base + s_off] = make_uint2(NONE, NONE);
   }
-  flush_slots(s_db, s_rec, Sn, Slon, B.Sd[1], B.Srec[1]);
+  if (threadIdx.x < 4) {  // this CTA's records -> its row (no contention)
+    SlotRec o = s_rec[threadIdx.x];
+    if (threadIdx.x >= Sn) o.id = NONE;
+    o.lock = 0u;
+    B.Rc[1][(size_t)blockIdx.x * NSLOT + threadIdx.x] = o;
+  }
   if (threadIdx.x == 0) B.run_cnt[1][blockIdx.x] = s_off;
 
   // ---- last CTA closes round 1 ----
@@ -439,6 +490,38 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   if (!s_last) return;
   __threadfence();
   const uint32_t mn = sum_runs(B.run_cnt[1], gridDim.x, s_ws);
+  {  // the farthest record of each segment over the CTAs' rows -> Srec[1]
+    __shared__ unsigned long long s_best4[4][4];
+    Cand a[4];
+    unsigned long long key[4][4];
+    bool valid[4], win[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      a[t] = empty_cand();
+      if (threadIdx.x < gridDim.x) {
+        const SlotRec* q = B.Rc[1] + (size_t)threadIdx.x * NSLOT + t;
+        a[t].id = __ldcg(&q->id);
+        if (a[t].id != NONE) {
+          a[t].d = __ldcg(&q->d);
+          a[t].x = __ldcg(&q->x);
+          a[t].y = __ldcg(&q->y);
+        }
+      }
+      a[t].pos = 0;
+      cand_keys(a[t], (uint32_t)t < Slon, key[t]);
+      valid[t] = a[t].id != NONE;
+    }
+    cta_lexmin<4, 4>(key, valid, s_best4, win);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (win[t]) {
+        SlotRec o;
+        o.d = a[t].d; o.x = a[t].x; o.y = a[t].y; o.id = a[t].id; o.lock = 0u;
+        B.Srec[1][t] = o;
+        B.Sd[1][t] = (unsigned long long)__double_as_longlong(a[t].d);
+      }
+    }
+  }
   if (threadIdx.x != 0) return;
   c->ticket = 0;
   const uint32_t before = c->S_cur + c->m_cur;
@@ -516,25 +599,53 @@ SH_DEV void write_heads(const Bufs& B, uint32_t pin, uint32_t pout, const Route&
   }
 }
 
+// Where the farthest records of the current segments are: this CTA's shared
+// slots (a lone CTA kept them), the global records Srec (written by K3, the
+// small-input kernel or the solo tail), or the CTA rows of a multi-CTA round,
+// resolved through the winner words Wn.
+enum : uint32_t { RS_SMEM = 0, RS_SREC = 1, RS_ROWS = 2 };
+struct RecSrc {
+  uint32_t kind;
+  const SlotRec* base;  // sm.rec, Srec[sin] or Rc[parity of the previous round]
+  const uint32_t* wn;   // RS_ROWS: Wn[sin]
+};
+
+// record of segment s, or nullptr when it has none (RS_ROWS without winner)
+SH_DEV const SlotRec* rec_at(const RecSrc& rs, uint32_t s) {
+  if (rs.kind != RS_ROWS) return rs.base + s;
+  const uint32_t w = __ldcg(rs.wn + s);
+  return w == NONE ? nullptr : rs.base + (size_t)w * NSLOT + s;
+}
+SH_DEV uint32_t rec_id(const SlotRec* r) {
+  return r == nullptr ? NONE : (__isShared(r) ? r->id : __ldcg(&r->id));
+}
+
 // Small table (S <= SMALL_S), rebuilt by every participating CTA in smem.
 // CTA 0 also writes the next head table.  The farthest records of the
 // current segments come from the global slots, or -- when the previous round
 // ran on this single CTA -- straight from its shared-memory slots.
 // Returns S', S'lo.
 SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, uint32_t pin,
-                        uint32_t pout, uint32_t sin, bool from_smem, uint32_t* s_ws,
+                        uint32_t pout, const RecSrc& rs, uint32_t* s_ws,
                         uint32_t& Sn, uint32_t& Slon) {
+  __shared__ SlotRec s_none;  // stands for "no record" in make_route
+  if (threadIdx.x == 0) {
+    s_none.d = s_none.x = s_none.y = 0.0;
+    s_none.id = NONE;
+    s_none.lock = 0u;
+  }
+  __syncthreads();
   const bool heads = blockIdx.x == 0;
-  const SlotRec* recs = from_smem ? sm.rec : B.Srec[sin];
   uint32_t running = 0, lower_splits = 0;
   for (uint32_t s0 = 0; s0 < S; s0 += RTPB) {
     const uint32_t s = s0 + threadIdx.x;
-    const uint32_t split = (s < S && (from_smem ? recs[s].id : __ldcg(&recs[s].id)) != NONE) ? 1u : 0u;
+    const SlotRec* cr = s < S ? rec_at(rs, s) : nullptr;
+    const uint32_t split = rec_id(cr) != NONE ? 1u : 0u;
     uint32_t total;
     const uint32_t pre = block_exclusive_scan(split, s_ws, &total);
     lower_splits += (uint32_t)__syncthreads_count(split && s < Slo);
     if (s < S) {
-      const Route r = make_route(B, pin, recs + s, s, S, Slo, s + running + pre);
+      const Route r = make_route(B, pin, cr ? cr : &s_none, s, S, Slo, s + running + pre);
       sm.rt[s] = r;
       if (heads) write_heads(B, pin, pout, r, s);
     }
@@ -559,8 +670,8 @@ SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, 
 constexpr int TS = 8;
 
 SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, uint32_t pout,
-                        uint32_t sin, uint32_t sout, uint32_t P, bool from_rec, uint32_t* s_ws,
-                        uint32_t& Sn, uint32_t& Slon) {
+                        uint32_t sin, uint32_t sout, uint32_t P, bool from_rec, const RecSrc& rs,
+                        uint32_t* s_ws, uint32_t& Sn, uint32_t& Slon) {
   Ctl* c = B.ctl;
   constexpr uint32_t STEP = RTPB * TS;
   // CTA ranges are whole warp chunks (32 * TS), so that the lane mapping is
@@ -570,10 +681,9 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   const uint32_t lo = min(S, blockIdx.x * per), hi = min(S, lo + per);
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t* Win = B.Wn[sin];
-  const SlotRec* recs = B.Srec[sin];
   auto split_of = [&](uint32_t s) -> uint32_t {  // C's live position / record index, or NONE
     if (s >= hi) return NONE;
-    if (from_rec) return __ldcg(&recs[s].id) != NONE ? s : NONE;
+    if (from_rec) return rec_id(rec_at(rs, s)) != NONE ? s : NONE;
     return __ldcg(Win + s);
   };
   // T1: split counts of this CTA's range (total and lower chain)
@@ -679,9 +789,10 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
         bx[i] = __ldcg(Tx + sb);
         by[i] = __ldcg(Ty + sb);
         if (from_rec) {
-          cx[i] = __ldcg(&recs[s].x);
-          cy[i] = __ldcg(&recs[s].y);
-          cid[i] = __ldcg(&recs[s].id);
+          const SlotRec* cr = rec_at(rs, s);  // global (RS_SREC or RS_ROWS), a winner exists
+          cx[i] = __ldcg(&cr->x);
+          cy[i] = __ldcg(&cr->y);
+          cid[i] = __ldcg(&cr->id);
         } else {
           const double2 cv = __ldcg(B.Lxy[pin] + w[i]);
           cx[i] = cv.x;
@@ -738,7 +849,7 @@ struct SoloState {
 // Returns true when the call is finished (control block written), false when
 // the table outgrew SMALL_S: the state is then exported to global memory (one
 // run, records in Srec) and the caller continues with the grid-wide rounds.
-SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, bool recs_smem,
+SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSrc& rs,
                         uint32_t* s_ws, uint32_t* s_pref, uint32_t* s_off) {
   Ctl* c = B.ctl;
   const uint32_t tid = threadIdx.x, q = B.run_q, n = B.n;
@@ -749,18 +860,22 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, bool recs_s
   uint32_t r = st.r, S = st.S, Slo = st.Slo, m = st.m;
   const unsigned long long t0 = *(volatile unsigned long long*)&c->t0_ns;
   {  // ---- import: heads, records (unless already here), live set ----
-    const uint32_t pin = (r - 1) & 1u, sin = (r - 1) % 3u;
+    const uint32_t pin = (r - 1) & 1u;
     for (uint32_t s = tid; s < S; s += RTPB) {
       hxy[s] = make_double2(__ldcg(B.Tx[pin] + s), __ldcg(B.Ty[pin] + s));
       hid[s].x = __ldcg(B.Tid[pin] + s);
-      if (!recs_smem) {
-        sm.db[s] = __ldcg(B.Sd[sin] + s);
-        const SlotRec* g = B.Srec[sin] + s;
-        sm.rec[s].d = __ldcg(&g->d);
-        sm.rec[s].x = __ldcg(&g->x);
-        sm.rec[s].y = __ldcg(&g->y);
-        sm.rec[s].id = __ldcg(&g->id);
-        sm.rec[s].lock = 0u;
+      if (rs.kind != RS_SMEM) {
+        const SlotRec* g = rec_at(rs, s);
+        if (rec_id(g) == NONE) {
+          rec_clear(&sm.db[s], &sm.rec[s]);
+        } else {
+          sm.rec[s].d = __ldcg(&g->d);
+          sm.rec[s].x = __ldcg(&g->x);
+          sm.rec[s].y = __ldcg(&g->y);
+          sm.rec[s].id = __ldcg(&g->id);
+          sm.rec[s].lock = 0u;
+          sm.db[s] = (unsigned long long)__double_as_longlong(sm.rec[s].d);
+        }
       }
     }
     const uint32_t nruns = st.nruns;
@@ -958,8 +1073,15 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   const uint32_t n = B.n, q = B.run_q;
   const uint32_t target = min(ROUND_TARGET, q);
   uint32_t P = gridDim.x;
-  bool recs_smem = false;  // this round's input records live in this CTA's smem
-  bool prev_small = true;  // the previous round used a small table (records in Srec)
+  uint32_t rec_kind = RS_SREC;  // where this round's input records are (RecSrc)
+  auto rec_src = [&](uint32_t kind, uint32_t rr) {
+    RecSrc rs;
+    rs.kind = kind;
+    rs.wn = B.Wn[(rr - 1) % 3u];
+    rs.base = kind == RS_SMEM ? sm.rec : kind == RS_SREC ? B.Srec[(rr - 1) % 3u] : B.Rc[(rr - 1) & 1u];
+    return rs;
+  };
+  bool prev_small = true;  // the previous round used a small table
   uint32_t kbase = 0;      // live tiles this CTA consumed in earlier rounds
   if (blockIdx.x == 0 && threadIdx.x == 0) c->mark[5] = globaltimer_ns() - c->t0_ns;
   unsigned long long t_table = 0, t_points = 0;  // CTA 0 phase timestamps
@@ -987,13 +1109,14 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     KR_MARK();  // round start
     if (P == 1 && S <= (uint32_t)SMALL_S && m + nruns <= SOLO_CAP) {
       SoloState ss{r, S, Slo, m, nruns};
-      if (solo_rounds(B, sm, ss, recs_smem, s_ws, s_pref, &s_off)) return;
+      const RecSrc rs0 = rec_src(rec_kind, r);
+      if (solo_rounds(B, sm, ss, rs0, s_ws, s_pref, &s_off)) return;
       r = ss.r;
       S = ss.S;
       Slo = ss.Slo;
       m = ss.m;
       nruns = ss.nruns;
-      recs_smem = false;
+      rec_kind = RS_SREC;  // the solo tail exported its records to Srec
       prev_small = true;
       continue;
     }
@@ -1002,8 +1125,9 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     const bool small = S <= (uint32_t)SMALL_S;
     uint32_t Sn, Slon;
     if (small) {
-      table_small(B, sm, S, Slo, pin, pout, sin, recs_smem, s_ws, Sn, Slon);
-    } else if (!table_large(B, S, Slo, pin, pout, sin, sout, P, prev_small, s_ws, Sn, Slon)) {
+      table_small(B, sm, S, Slo, pin, pout, rec_src(rec_kind, r), s_ws, Sn, Slon);
+    } else if (!table_large(B, S, Slo, pin, pout, sin, sout, P, prev_small, rec_src(rec_kind, r),
+                            s_ws, Sn, Slon)) {
       return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) t_table = globaltimer_ns();
@@ -1012,8 +1136,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     // round r+1 will use a small table; a large table clears its own slots
     if (Sn <= (uint32_t)SMALL_S) {
       const uint32_t lim = min(2 * Sn, B.s_cap);
-      for (uint32_t t = blockIdx.x * RTPB + threadIdx.x; t < lim; t += P * RTPB)
+      for (uint32_t t = blockIdx.x * RTPB + threadIdx.x; t < lim; t += P * RTPB) {
         rec_clear(B.Sd[sres] + t, B.Srec[sres] + t);
+        B.Wn[sres][t] = NONE;
+      }
     }
     // prefix of the input run counts: the live set as one virtual range
     {
@@ -1041,7 +1167,6 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     double2* Oxy = B.Lxy[pout];
     uint2* Ois = B.Lis[pout];
     unsigned long long* Sd = B.Sd[sout];
-    SlotRec* Srec = B.Srec[sout];
     const uint32_t obase = blockIdx.x * q;
     const uint32_t Mp = s_pref[nruns];
     const uint32_t lo = 2u * (uint32_t)((unsigned long long)(Mp / 2) * blockIdx.x / P);
@@ -1180,13 +1305,17 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     }
     // a lone CTA whose next table is small keeps its records in smem
     const bool keep_smem = small && P == 1 && Sn <= (uint32_t)SMALL_S;
-    if (small && !keep_smem) flush_slots(sm.db, sm.rec, Sn, Slon, Sd, Srec);
+    if (small && !keep_smem) flush_rows(sm.db, sm.rec, Sn, Sd, B.Rc[r & 1u] + (size_t)blockIdx.x * NSLOT);
     if (threadIdx.x == 0) B.run_cnt[pout][blockIdx.x] = s_off;
     if (blockIdx.x == 0 && threadIdx.x == 0) t_points = globaltimer_ns();
     if (threadIdx.x == 0 && r == trace_r) B.dbg[blockIdx.x] = globaltimer_ns() - c->t0_ns;
     KR_MARK();  // slots flushed
     rounds_barrier(c, P);
     KR_MARK();  // barrier passed
+    if (small && !keep_smem) {  // rows at the final maxima claim their slots
+      claim_slots(sm.rec, Sn, Slon, Sd, B.Wn[sout], B.Rc[r & 1u]);
+      rounds_barrier(c, P);
+    }
     if (!small) {
       // winner pass over this CTA's contenders (listed in its run's slice of
       // Lc, still hot in L2): the ones whose distance equals their segment's
@@ -1255,7 +1384,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     Slo = Slon;
     m = mn;
     nruns = P;
-    recs_smem = keep_smem;
+    rec_kind = small ? (keep_smem ? RS_SMEM : RS_ROWS) : RS_SREC;
     prev_small = small;
     if (mn == 0 || r + 1 > n) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -178,6 +178,9 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
     o_wn[p] = take(4 * S);
   }
   const size_t o_lc = take(sizeof(LiveCand) * LN);
+  const size_t rows = (size_t)std::max(ws->rounds_grid, ws->stream_grid);
+  const size_t o_rc0 = take(sizeof(SlotRec) * NSLOT * rows);
+  const size_t o_rc1 = take(sizeof(SlotRec) * NSLOT * rows);
   const size_t o_route = take(sizeof(Route) * S);
   CK(cudaMalloc(&ws->arena, off));
   char* a = (char*)ws->arena;
@@ -208,6 +211,8 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
     B.Wn[p] = (uint32_t*)(a + o_wn[p]);
   }
   B.Lc = (LiveCand*)(a + o_lc);
+  B.Rc[0] = (SlotRec*)(a + o_rc0);
+  B.Rc[1] = (SlotRec*)(a + o_rc1);
   B.route = (Route*)(a + o_route);
   B.s_cap = (uint32_t)std::min<uint64_t>(s_cap, 0xFFFFFFF0ull);
   return ws;
