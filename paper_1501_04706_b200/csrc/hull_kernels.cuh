@@ -35,7 +35,10 @@ namespace shb {
 
 constexpr int TPB = 256;             // K1 / K2 / K3 (streaming kernels)
 constexpr int WARPS = TPB / 32;
-constexpr int RTPB = 512;            // persistent round kernel
+#ifndef SHB_RTPB
+#define SHB_RTPB 512
+#endif
+constexpr int RTPB = SHB_RTPB;       // persistent round kernel
 // TMA-fed streaming kernels K1/K2/K3: one CTA per SM, warp CW is the TMA
 // producer, warps 0..CW-1 consume CH 64-point chunks each per tile.
 template <int TPB_, int CH_, int NS_>

@@ -667,7 +667,10 @@ SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, 
 // head copy; only split ones build a route row and prepare the two winner
 // slots / distance maxima of their children.  Returns false on segment-table
 // overflow (every CTA returns consistently).
-constexpr int TS = 8;
+#ifndef SHB_TS
+#define SHB_TS 8
+#endif
+constexpr int TS = SHB_TS;
 
 SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, uint32_t pout,
                         uint32_t sin, uint32_t sout, uint32_t P, bool from_rec, const RecSrc& rs,
@@ -1043,7 +1046,7 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
   }
 }
 
-constexpr uint32_t ROUND_TARGET = 4 * RCTHREADS;  // live points per active CTA before CTAs retire
+constexpr uint32_t ROUND_TARGET = 1920;  // live points per active CTA before CTAs retire
 #ifndef SHB_KR_REVERSE
 #define SHB_KR_REVERSE 1
 #endif
