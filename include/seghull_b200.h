@@ -44,6 +44,9 @@ enum sh_status {
   SH_DEGENERATE_INPUT = 3,    /* Errc::DegenerateInput hull.cpp:108-110  */
   SH_INPUT_TOO_LARGE = 4,     /* Errc::InputTooLarge   (n >= 2^32 here)  */
   SH_INTERNAL_ERROR = 5,      /* Errc::InternalError   hull.cpp:265-267  */
+  SH_FILE_NOT_FOUND = 6,      /* Errc::FileNotFound    dataio.cpp:84-86  */
+  SH_PARSE_ERROR = 7,         /* Errc::ParseError      dataio.cpp:117-134 */
+  SH_IO_ERROR = 9,            /* Errc::IoError         dataio.cpp:88      */
   SH_CAP_TOO_SMALL = 100,     /* out buffers too small; *out_h = needed  */
   SH_CUDA_ERROR = 101,        /* CUDA runtime error (no device, OOM, ...) */
   SH_INVALID_ARGUMENT = 102
@@ -159,6 +162,21 @@ int sh_b200_gen_disk(double* x, double* y, uint64_t n, uint64_t seed, int device
  * from the host libm, because device cos/sin are not bit-identical to glibc.
  * Circle inputs are therefore generated on the host and uploaded. */
 int sh_b200_gen_circle_host(double* x, double* y, uint64_t n, uint64_t seed);
+
+/*
+ * PTS2 binary point file straight to HBM,
+ * replacing seghull::read_points_binary (dataio.cpp:114-153; layout: "PTS2",
+ * u64 LE count, then count x {f64 LE x, f64 LE y}).  The file is read in
+ * chunks into pinned host buffers, copied to the device and split into the
+ * caller's device arrays x[count], y[count] on `stream`, overlapping the
+ * file read with the transfer.  x == NULL or y == NULL: only *n = count.
+ * Returns SH_OK, SH_CAP_TOO_SMALL (cap < count; *n = count),
+ * SH_FILE_NOT_FOUND, SH_IO_ERROR, SH_PARSE_ERROR (truncated header, bad
+ * magic, size != 12 + 16 count) or SH_NON_FINITE_INPUT ("non-finite
+ * coordinate at point i", the first such i) with the reference's messages.
+ */
+int sh_b200_read_pts2(const char* path, int device, void* stream, double* x, double* y,
+                      uint64_t cap, uint64_t* n, char* err, size_t errlen);
 
 /* Library/device information; returns SH_OK or SH_CUDA_ERROR. */
 int sh_b200_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,

@@ -138,6 +138,10 @@ def ref():
         L.ref_preprocess_discards.argtypes = [vp, vp, _u64]
         L.ref_preprocess_discards.restype = _u64
         L.ref_monotone_chain.argtypes = [vp, vp, _u64, vp, vp, vp]
+        L.ref_write_points_binary.argtypes = [ctypes.c_char_p, vp, vp, _u64, ctypes.c_char_p,
+                                              ctypes.c_size_t]
+        L.ref_read_points_binary.argtypes = [ctypes.c_char_p, vp, vp, _u64, vp, ctypes.c_char_p,
+                                             ctypes.c_size_t]
         _ref = L
     return _ref
 
@@ -316,3 +320,22 @@ def ref_monotone_chain(x, y):
     if rc:
         raise OracleError(rc)
     return ox[:h.value].copy(), oy[:h.value].copy()
+
+
+def ref_write_points_binary(path, x, y):
+    """The reference's PTS2 writer (dataio.cpp:319-345); returns (status, message)."""
+    x, y = _xy(x, y)
+    err = ctypes.create_string_buffer(512)
+    rc = ref().ref_write_points_binary(str(path).encode(), _ptr(x), _ptr(y), x.size, err, 512)
+    return rc, err.value.decode(errors="replace")
+
+
+def ref_read_points_binary(path, cap=1 << 24):
+    """The reference's PTS2 reader (dataio.cpp:114-153): (status, message, x, y)."""
+    x = np.empty(cap, np.float64)
+    y = np.empty(cap, np.float64)
+    n = ctypes.c_uint64(0)
+    err = ctypes.create_string_buffer(512)
+    rc = ref().ref_read_points_binary(str(path).encode(), _ptr(x), _ptr(y), cap, ctypes.byref(n),
+                                      err, 512)
+    return rc, err.value.decode(errors="replace"), x[:n.value].copy(), y[:n.value].copy()

@@ -136,4 +136,34 @@ int ref_monotone_chain(const double* x, const double* y, std::uint64_t n, double
   }
 }
 
+// seghull::write_points(..., PointFormat::Binary) / read_points_binary
+// (dataio.cpp:114-153, 319-345): the reference's own PTS2 writer and reader.
+int ref_write_points_binary(const char* path, const double* x, const double* y, std::uint64_t n,
+                            char* err, std::size_t errlen) {
+  try {
+    write_points(make_set(x, y, n), path, PointFormat::Binary);
+    return 0;
+  } catch (const Error& e) {
+    put_err(err, errlen, e.what());
+    return 1 + static_cast<int>(e.code());
+  }
+}
+
+int ref_read_points_binary(const char* path, double* x, double* y, std::uint64_t cap,
+                           std::uint64_t* n, char* err, std::size_t errlen) {
+  try {
+    const PointSet p = read_points(path, PointFormat::Binary);
+    *n = p.size();
+    if (p.size() > cap) return 100;
+    for (std::size_t i = 0; i < p.size(); ++i) {
+      x[i] = p.x[i];
+      y[i] = p.y[i];
+    }
+    return 0;
+  } catch (const Error& e) {
+    put_err(err, errlen, e.what());
+    return 1 + static_cast<int>(e.code());
+  }
+}
+
 }  // extern "C"

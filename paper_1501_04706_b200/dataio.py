@@ -96,3 +96,60 @@ def gen_disk_device(n: int, seed: int, device: int = 0, stream=None):
     if rc:
         raise RuntimeError(f"sh_b200_gen_disk failed ({rc})")
     return x, y
+
+
+# ---------------------------------------------------------------------------
+# PTS2 binary point files (dataio.cpp:114-153 read, 319-345 write):
+# "PTS2", u64 LE count, then count x {f64 LE x, f64 LE y}.
+# ---------------------------------------------------------------------------
+
+_PTS2 = b"PTS2"
+_PTS2_DTYPE = np.dtype([("x", "<f8"), ("y", "<f8")])
+
+
+def write_points_binary(path, x, y) -> None:
+    """seghull::write_points(..., PointFormat::Binary) (dataio.cpp:319-345)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if x.shape != y.shape:
+        raise ValueError("x and y differ in length")
+    rec = np.empty(x.size, _PTS2_DTYPE)
+    rec["x"] = x
+    rec["y"] = y
+    try:
+        with open(path, "wb") as f:
+            f.write(_PTS2)
+            f.write(int(x.size).to_bytes(8, "little"))
+            rec.tofile(f)
+    except OSError as e:
+        from .hull import Errc, Error
+        raise Error(Errc.IoError, f"cannot open for writing: {path}") from e
+
+
+def read_points_binary_device(path, device: int = 0, stream=None):
+    """PTS2 file -> (x, y) float64 CUDA tensors, read straight to HBM by the
+    library (sh_b200_read_pts2: pinned double-buffered chunks, device split).
+    Errors as seghull::read_points_binary: hull.Error with Errc.FileNotFound,
+    IoError, ParseError or NonFiniteInput and the reference's messages."""
+    import ctypes
+
+    import torch
+
+    from .hull import _raise
+    L = _lib.load()
+    n = ctypes.c_uint64(0)
+    err = ctypes.create_string_buffer(512)
+    p = str(path).encode()
+    rc = L.sh_b200_read_pts2(p, device, None, None, None, 0, ctypes.byref(n), err, 512)
+    if rc:
+        _raise(rc, err.value.decode(errors="replace"))
+    dev = torch.device("cuda", device)
+    x = torch.empty(n.value, dtype=torch.float64, device=dev)
+    y = torch.empty(n.value, dtype=torch.float64, device=dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    rc = L.sh_b200_read_pts2(p, device, stream, x.data_ptr(), y.data_ptr(), n.value,
+                             ctypes.byref(n), err, 512)
+    if rc:
+        _raise(rc, err.value.decode(errors="replace"))
+    return x, y

@@ -145,8 +145,7 @@ class HullResult:
         return int(self.x.size)
 
 
-_ERRC_OF_STATUS = {1: Errc.EmptyInput, 2: Errc.NonFiniteInput, 3: Errc.DegenerateInput,
-                   4: Errc.InputTooLarge, 5: Errc.InternalError}
+_ERRC_OF_STATUS = {1 + int(e): e for e in Errc}  # status = 1 + Errc (include/seghull_b200.h)
 
 
 def _raise(rc: int, msg: str):
