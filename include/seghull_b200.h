@@ -178,6 +178,19 @@ int sh_b200_gen_circle_host(double* x, double* y, uint64_t n, uint64_t seed);
 int sh_b200_read_pts2(const char* path, int device, void* stream, double* x, double* y,
                       uint64_t cap, uint64_t* n, char* err, size_t errlen);
 
+/*
+ * hull::preprocess as a device API (hull.hpp:61-64,
+ * hull.cpp:53-99): the points outside the strict interior of the quadrilateral
+ * of the four extremes, in input order, written to out_x/out_y (device, cap
+ * entries; NULL = count only).  *kept = survivors, *discarded = n - kept.
+ * x, y are device arrays.  Returns SH_OK, SH_EMPTY_INPUT, SH_CAP_TOO_SMALL,
+ * SH_NON_FINITE_INPUT (first bad index; the reference does not check here)
+ * or SH_CUDA_ERROR.
+ */
+int sh_b200_preprocess(const double* x, const double* y, uint64_t n, int device, void* stream,
+                       double* out_x, double* out_y, uint64_t cap, uint64_t* kept,
+                       uint64_t* discarded, char* err, size_t errlen);
+
 /* Library/device information; returns SH_OK or SH_CUDA_ERROR. */
 int sh_b200_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                         uint64_t* hbm_bytes, char* name, size_t namelen);

@@ -138,6 +138,7 @@ def ref():
         L.ref_preprocess_discards.argtypes = [vp, vp, _u64]
         L.ref_preprocess_discards.restype = _u64
         L.ref_monotone_chain.argtypes = [vp, vp, _u64, vp, vp, vp]
+        L.ref_preprocess.argtypes = [vp, vp, _u64, vp, vp, vp, vp]
         L.ref_write_points_binary.argtypes = [ctypes.c_char_p, vp, vp, _u64, ctypes.c_char_p,
                                               ctypes.c_size_t]
         L.ref_read_points_binary.argtypes = [ctypes.c_char_p, vp, vp, _u64, vp, ctypes.c_char_p,
@@ -339,3 +340,16 @@ def ref_read_points_binary(path, cap=1 << 24):
     rc = ref().ref_read_points_binary(str(path).encode(), _ptr(x), _ptr(y), cap, ctypes.byref(n),
                                       err, 512)
     return rc, err.value.decode(errors="replace"), x[:n.value].copy(), y[:n.value].copy()
+
+
+def ref_preprocess(x, y):
+    """The reference's hull::preprocess: (kept_x, kept_y, discarded)."""
+    x, y = _xy(x, y)
+    ox = np.empty(max(x.size, 1), np.float64)
+    oy = np.empty(max(x.size, 1), np.float64)
+    k, d = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    rc = ref().ref_preprocess(_ptr(x), _ptr(y), x.size, _ptr(ox), _ptr(oy), ctypes.byref(k),
+                              ctypes.byref(d))
+    if rc:
+        raise OracleError(rc)
+    return ox[:k.value].copy(), oy[:k.value].copy(), int(d.value)

@@ -136,6 +136,23 @@ int ref_monotone_chain(const double* x, const double* y, std::uint64_t n, double
   }
 }
 
+// hull::preprocess (hull.hpp:64): the filtered set in input order.
+int ref_preprocess(const double* x, const double* y, std::uint64_t n, double* out_x,
+                   double* out_y, std::uint64_t* kept, std::uint64_t* discarded) {
+  try {
+    const auto r = hull::preprocess(make_set(x, y, n), Backend::Sequential);
+    *kept = r.first.size();
+    *discarded = r.second;
+    for (std::size_t i = 0; i < r.first.size(); ++i) {
+      out_x[i] = r.first.x[i];
+      out_y[i] = r.first.y[i];
+    }
+    return 0;
+  } catch (const Error& e) {
+    return 1 + static_cast<int>(e.code());
+  }
+}
+
 // seghull::write_points(..., PointFormat::Binary) / read_points_binary
 // (dataio.cpp:114-153, 319-345): the reference's own PTS2 writer and reader.
 int ref_write_points_binary(const char* path, const double* x, const double* y, std::uint64_t n,

@@ -51,7 +51,8 @@ class sh_hull_result(ctypes.Structure):
 # every symbol include/seghull_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sh_b200_hull", "sh_b200_hull_ex", "sh_b200_gen_uniform", "sh_b200_gen_disk",
            "sh_b200_gen_circle_host", "sh_b200_device_info", "sh_b200_release_pool",
-           "sh_b200_abi_version", "sh_b200_read_pts2")
+           "sh_b200_abi_version", "sh_b200_read_pts2",
+           "sh_b200_preprocess")
 
 SH_HOST_PTRS = 0
 SH_DEVICE_PTRS = 1
@@ -83,6 +84,9 @@ def load() -> ctypes.CDLL:
     L.sh_b200_read_pts2.argtypes = [ctypes.c_char_p, ctypes.c_int, _vp, _vp, _vp, _u64, _vp,
                                     ctypes.c_char_p, ctypes.c_size_t]
     L.sh_b200_read_pts2.restype = ctypes.c_int
+    L.sh_b200_preprocess.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp, _vp, _vp, _u64, _vp, _vp,
+                                     ctypes.c_char_p, ctypes.c_size_t]
+    L.sh_b200_preprocess.restype = ctypes.c_int
     L.sh_b200_release_pool.argtypes = []
     L.sh_b200_release_pool.restype = None
     L.sh_b200_abi_version.restype = ctypes.c_int

@@ -291,6 +291,44 @@ SH_DEV void cand_visit(Cand& a, double d, double x, double y, uint32_t id, uint3
   }
 }
 
+// Every CTA of the kernel after K1 combines K1's per-CTA extremes into the
+// quadrilateral (Fin, in shared memory); with `publish`, CTA 0 also writes it
+// to the control block and clears round 1's farthest slots.  Contains barriers.
+SH_DEV void combine_k1(const Bufs& B, Fin& s_fin, bool publish) {
+  Ctl* c = B.ctl;
+  ExtRec e[4];
+  unsigned long long bad = ~0ull;
+  for (int k = 0; k < 4; ++k) e[k].id = e[k].pos = NONE;
+  if (threadIdx.x < B.k1_grid) {
+    const K1Partial* qp = B.k1part + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      e[k].x = __ldcg(&qp->e[k].x);
+      e[k].y = __ldcg(&qp->e[k].y);
+      e[k].id = __ldcg(&qp->e[k].id);
+      e[k].pos = __ldcg(&qp->e[k].pos);
+    }
+    bad = __ldcg(&qp->bad);
+  }
+  __shared__ ExtRec s_ext[4];
+  __shared__ unsigned long long s_bad;
+  cta_extremes(e, bad, s_ext, &s_bad);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const ExtRec ee[4] = {s_ext[0], s_ext[1], s_ext[2], s_ext[3]};
+    compute_fin(s_fin, ee, s_bad);
+    if (publish && blockIdx.x == 0) {
+      write_fin(c, s_fin);
+      const unsigned long long now = globaltimer_ns() - c->t0_ns;
+      c->mark[0] = now;
+      c->mark[1] = now;
+      // round 1 (K3) offers its farthest points into Slot[1] (<= 4 segments)
+      for (int t = 0; t < 4; ++t) rec_clear(&B.Sd[1][t], &B.Srec[1][t]);
+    }
+  }
+  __syncthreads();
+}
+
 template <bool FILTER, bool IDS>
 __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -302,39 +340,7 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   // ---- every CTA combines K1's per-CTA extremes (no serial last-CTA step) ----
   __shared__ Fin s_fin;
-  {
-    ExtRec e[4];
-    unsigned long long bad = ~0ull;
-    for (int k = 0; k < 4; ++k) e[k].id = e[k].pos = NONE;
-    if (threadIdx.x < B.k1_grid) {
-      const K1Partial* qp = B.k1part + threadIdx.x;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        e[k].x = __ldcg(&qp->e[k].x);
-        e[k].y = __ldcg(&qp->e[k].y);
-        e[k].id = __ldcg(&qp->e[k].id);
-        e[k].pos = __ldcg(&qp->e[k].pos);
-      }
-      bad = __ldcg(&qp->bad);
-    }
-    __shared__ ExtRec s_ext[4];
-    __shared__ unsigned long long s_bad;
-    cta_extremes(e, bad, s_ext, &s_bad);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const ExtRec ee[4] = {s_ext[0], s_ext[1], s_ext[2], s_ext[3]};
-      compute_fin(s_fin, ee, s_bad);
-      if (blockIdx.x == 0) {
-        write_fin(c, s_fin);
-        const unsigned long long now = globaltimer_ns() - c->t0_ns;
-        c->mark[0] = now;
-        c->mark[1] = now;
-        // round 1 (K3) offers its farthest points into Slot[1] (<= 4 segments)
-        for (int t = 0; t < 4; ++t) rec_clear(&B.Sd[1][t], &B.Srec[1][t]);
-      }
-    }
-    __syncthreads();
-  }
+  combine_k1(B, s_fin, true);
   if (s_fin.status != ST_RUNNING) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n = B.n;
@@ -746,6 +752,127 @@ cudaError_t configure_stream_kernels_pre() {
   e = cudaFuncSetAttribute(k2_classify<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring2<true>::kBytes);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k2_classify<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ring2<true>::kBytes);
+}
+
+// ===========================================================================
+// KP: hull::preprocess as a device API (hull.hpp:61-64, hull.cpp:53-99):
+// K1's extremes, then every point outside the quadrilateral's strict interior
+// is kept, compacted STABLY (input order, like stable_partition_by_flag) with
+// a decoupled look-back over 2048-point tiles taken from a tile counter.
+// Degenerate quadrilaterals (< 3 distinct corners) keep every point.
+// ===========================================================================
+
+constexpr int KP_TPB = 256, KP_ITEMS = 8, KP_TILE = KP_TPB * KP_ITEMS;
+
+__global__ void __launch_bounds__(KP_TPB) k_preprocess(Bufs B, double* ox, double* oy,
+                                                        unsigned long long cap) {
+  Ctl* c = B.ctl;
+  __shared__ Fin s_fin;
+  combine_k1(B, s_fin, false);
+  const uint32_t st = s_fin.status;
+  if (st == ST_NONFINITE) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      c->status = ST_NONFINITE;
+      c->bad_index = s_fin.bad;
+    }
+    return;
+  }
+  const bool filt = st == ST_RUNNING && s_fin.distinct >= 3;
+  const int ne = filt ? s_fin.nedges : 0;
+  Edge Q[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    Q[k].ax = s_fin.edges[k][0];
+    Q[k].ay = s_fin.edges[k][1];
+    Q[k].ex = s_fin.edges[k][2];
+    Q[k].ey = s_fin.edges[k][3];
+  }
+  __shared__ uint32_t s_cnt[KP_ITEMS * (KP_TPB / 32)];
+  __shared__ uint32_t s_tile, s_prefix;
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int W = KP_TPB / 32;
+  const uint32_t epoch = *(volatile uint32_t*)B.epoch;
+  const uint32_t n = B.n;
+  const uint32_t ntiles = (n + KP_TILE - 1) / KP_TILE;
+  while (true) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&c->tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    double px[KP_ITEMS], py[KP_ITEMS];
+    uint32_t keep = 0, rank[KP_ITEMS];
+#pragma unroll
+    for (int j = 0; j < KP_ITEMS; ++j) {
+      const uint32_t i = tile * KP_TILE + j * KP_TPB + threadIdx.x;
+      if (i < n) {
+        px[j] = __ldcs(B.in_x + i);
+        py[j] = __ldcs(B.in_y + i);
+        bool inside = filt;  // hull.cpp:80-90: discard iff cross > 0 for every edge
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < ne) inside = inside & (cross_e(Q[k], px[j], py[j]) > 0.0);
+        if (!inside) keep |= 1u << j;
+      }
+      const unsigned bal = __ballot_sync(FULL, (keep >> j) & 1u);
+      if (lane == 0) s_cnt[j * W + warp] = __popc(bal);
+      rank[j] = __popc(bal & lanemask_lt());
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the KP_ITEMS x W warp counts (j-major)
+      uint32_t v[KP_ITEMS * W / 32];
+      uint32_t sum = 0;
+#pragma unroll
+      for (int q = 0; q < KP_ITEMS * W / 32; ++q) {
+        v[q] = s_cnt[lane * (KP_ITEMS * W / 32) + q];
+        sum += v[q];
+      }
+      uint32_t incl = sum;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int q = 0; q < KP_ITEMS * W / 32; ++q) {
+        s_cnt[lane * (KP_ITEMS * W / 32) + q] = run;
+        run += v[q];
+      }
+      const uint32_t agg = __shfl_sync(FULL, incl, 31);
+      const uint32_t p = lookback_warp(B.tile_status, tile, agg, epoch);
+      if (lane == 0) {
+        s_prefix = p;
+        if (tile == ntiles - 1) c->m_next = p + agg;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < KP_ITEMS; ++j) {
+      if ((keep >> j) & 1u) {
+        const unsigned long long o = (unsigned long long)s_prefix + s_cnt[j * W + warp] + rank[j];
+        if (o < cap) {
+          ox[o] = px[j];
+          oy[o] = py[j];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&c->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    c->ticket = 0;
+    c->tile_ctr = 0;
+    *B.epoch = epoch + 1;
+    __threadfence();
+  }
+}
+
+void launch_preprocess(const Bufs& B, double* ox, double* oy, unsigned long long cap, int grid,
+                       cudaStream_t s) {
+  k_preprocess<<<grid, KP_TPB, 0, s>>>(B, ox, oy, cap);
 }
 
 void launch_small(const Bufs& B, bool filter, bool ids, cudaStream_t s) {

@@ -40,6 +40,8 @@ void launch_gen_disk(double* x, double* y, unsigned long long n, unsigned long l
                      Ctl* c, unsigned long long* status, uint32_t* epoch, int grid,
                      cudaStream_t s);
 int gen_tile_points();
+void launch_preprocess(const Bufs& B, double* ox, double* oy, unsigned long long cap, int grid,
+                       cudaStream_t s);
 }  // namespace shb
 
 using namespace shb;
@@ -668,6 +670,80 @@ int sh_b200_gen_disk(double* x, double* y, uint64_t n, uint64_t seed, int device
     cudaSetDevice(prev);
     return SH_OK;
   } catch (const CudaFail&) {
+    cudaGetLastError();
+    cudaSetDevice(prev);
+    return SH_CUDA_ERROR;
+  }
+}
+
+int sh_b200_preprocess(const double* x, const double* y, uint64_t n, int device, void* stream,
+                       double* out_x, double* out_y, uint64_t cap, uint64_t* kept,
+                       uint64_t* discarded, char* err, size_t errlen) {
+  if (kept) *kept = 0;
+  if (discarded) *discarded = 0;
+  if (n == 0) {  // hull.cpp:55
+    put_err(err, errlen, "preprocess: empty point set");
+    return SH_EMPTY_INPUT;
+  }
+  if (!x || !y || !kept) {
+    put_err(err, errlen, "null argument");
+    return SH_INVALID_ARGUMENT;
+  }
+  if (n >= (1ull << 32) - (1ull << 20)) {
+    put_err(err, errlen, "preprocess: more than 2^32 - 2^20 points");
+    return SH_INPUT_TOO_LARGE;
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  std::unique_ptr<Workspace> ws;
+  try {
+    CK(cudaSetDevice(device));
+    ws = acquire(device, n);
+    cudaStream_t st = stream ? (cudaStream_t)stream : ws->stream;
+    Bufs B = ws->B;
+    // K1's bulk copies need 16-byte aligned inputs: stage unaligned ones
+    if ((uintptr_t)x % 16 || (uintptr_t)y % 16) {
+      ensure_stage(*ws, false);
+      B = ws->B;
+      double* sx = (double*)ws->stage;
+      double* sy = (double*)((char*)ws->stage + align_up(8 * ws->n_cap, 256));
+      CK(cudaMemcpyAsync(sx, x, 8 * n, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(sy, y, 8 * n, cudaMemcpyDeviceToDevice, st));
+      B.in_x = sx;
+      B.in_y = sy;
+    } else {
+      B.in_x = x;
+      B.in_y = y;
+    }
+    B.in_id = nullptr;
+    B.n = (uint32_t)n;
+    const int g1 = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + Cfg1::T - 1) / Cfg1::T,
+                                                                 (uint64_t)ws->stream_grid));
+    B.k1_grid = (uint32_t)g1;
+    CK(cudaMemsetAsync(B.ctl, 0, sizeof(Ctl), st));
+    launch_k1(B, false, g1, st);
+    launch_preprocess(B, out_x, out_y, out_x && out_y ? cap : 0, ws->stream_grid * 8, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ws->h_ctl, B.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const Ctl& c = *ws->h_ctl;
+    int rc = SH_OK;
+    if (c.status == ST_NONFINITE) {
+      put_err(err, errlen, "preprocess: non-finite coordinate at index " + std::to_string(c.bad_index));
+      rc = SH_NON_FINITE_INPUT;
+    } else {
+      *kept = c.m_next;
+      if (discarded) *discarded = n - c.m_next;
+      if ((out_x || out_y) && c.m_next > cap) {
+        put_err(err, errlen, "output capacity too small");
+        rc = SH_CAP_TOO_SMALL;
+      }
+    }
+    release(std::move(ws));
+    cudaSetDevice(prev);
+    return rc;
+  } catch (const CudaFail& f) {
+    put_err(err, errlen, std::string(f.what) + ": " + cudaGetErrorString(f.err));
     cudaGetLastError();
     cudaSetDevice(prev);
     return SH_CUDA_ERROR;

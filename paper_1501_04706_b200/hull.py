@@ -366,6 +366,30 @@ def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int |
                       int(res.kernel_launches), ends[0], ends[1])
 
 
+def preprocess_device(x, y, *, stream: int | None = None):
+    """hull::preprocess (hull.hpp:61-64, hull.cpp:53-99) on device tensors:
+    returns (kept_x, kept_y, discarded) -- the points outside the strict
+    interior of the extremes' quadrilateral, in input order."""
+    import torch
+    x, y, _, px, py, dx, n = _prepare(x, y, None)
+    if not dx:
+        raise ValueError("preprocess_device needs CUDA tensors")
+    L = _lib.load()
+    device = int(x.device.index)
+    if stream is None:
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+    ox = torch.empty(max(n, 1), dtype=torch.float64, device=x.device)
+    oy = torch.empty(max(n, 1), dtype=torch.float64, device=x.device)
+    kept, disc = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    err = ctypes.create_string_buffer(256)
+    rc = L.sh_b200_preprocess(px, py, n, device, stream, ox.data_ptr(), oy.data_ptr(), n,
+                              ctypes.byref(kept), ctypes.byref(disc), err, 256)
+    if rc:
+        _raise(rc, err.value.decode(errors="replace"))
+    k = int(kept.value)
+    return ox[:k], oy[:k], int(disc.value)
+
+
 def run(points: PointSet, mode: Mode = Mode.WithPreprocess,
         backend: Backend = Backend.B200) -> HullResult:
     """seghull::hull::run (hull.hpp:95) on the B200 backend."""
