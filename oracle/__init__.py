@@ -78,6 +78,10 @@ def build(with_ref: bool = True) -> None:
     targets = ["oracle"]
     if with_ref and os.path.isdir(REF_SRC):
         targets.append("ref")
+        # the reference's bench harness driving Backend::B200 (needs the product library)
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1501_04706_b200",
+                                       "libseghull_b200.so")):
+            targets.append("hullbench")
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 

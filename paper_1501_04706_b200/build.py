@@ -20,7 +20,8 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",                       # no FMA contraction on the device
-    "-Xcompiler", "-fPIC,-ffp-contract=off",  # ... nor on the host
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-fopenmp",  # ... nor on the host; OpenMP packs pageable H2D
+    "-lgomp",
     "-I", os.path.join(ROOT, "include"),
     "-shared",
 ]

@@ -284,6 +284,65 @@ struct RunOut {
   std::string msg;
 };
 
+// Host -> device copy of a caller's buffer.  Pinned (or registered) memory
+// goes straight to the copy engine.  Pageable memory would be staged by the
+// driver through one bounce buffer at ~11 GB/s; instead it is packed into
+// pinned chunks by all host cores (OpenMP) and the chunks are copied while
+// the next ones are packed (~4 chunk buffers in flight).
+constexpr size_t H2D_CHUNK = 8u << 20;
+constexpr int H2D_NBUF = 4;
+struct PinnedRing {
+  std::mutex mu;
+  char* buf[H2D_NBUF] = {};
+  cudaEvent_t done[H2D_NBUF] = {};
+  int dev = -1;
+};
+PinnedRing g_ring;
+
+void h2d_or_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, bool host,
+                 cudaStream_t st) {
+  if (!host || bytes < (H2D_CHUNK >> 2)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, kind, st));
+    return;
+  }
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+    CK(cudaMemcpyAsync(dst, src, bytes, kind, st));  // already pinned
+    return;
+  }
+  cudaGetLastError();  // pageable pointers may leave an error on older drivers
+  std::lock_guard<std::mutex> lk(g_ring.mu);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (!g_ring.buf[0]) {
+    for (int b = 0; b < H2D_NBUF; ++b) CK(cudaMallocHost((void**)&g_ring.buf[b], H2D_CHUNK));
+  }
+  if (g_ring.dev != dev) {  // events belong to a device
+    for (int b = 0; b < H2D_NBUF; ++b) {
+      if (g_ring.done[b]) cudaEventDestroy(g_ring.done[b]);
+      CK(cudaEventCreateWithFlags(&g_ring.done[b], cudaEventDisableTiming));
+      CK(cudaEventRecord(g_ring.done[b], st));
+    }
+    g_ring.dev = dev;
+  }
+  const char* s = (const char*)src;
+  char* d = (char*)dst;
+  for (size_t off = 0, k = 0; off < bytes; off += H2D_CHUNK, ++k) {
+    const int b = (int)(k % H2D_NBUF);
+    const size_t len = std::min(H2D_CHUNK, bytes - off);
+    CK(cudaEventSynchronize(g_ring.done[b]));  // the copy out of buf[b] finished
+    char* pb = g_ring.buf[b];
+    const long parts = 16;
+#pragma omp parallel for num_threads(8) schedule(static)
+    for (long t = 0; t < parts; ++t) {
+      const size_t a = len * t / parts, e = len * (t + 1) / parts;
+      std::memcpy(pb + a, s + off + a, e - a);
+    }
+    CK(cudaMemcpyAsync(d + off, pb, len, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(g_ring.done[b], st));
+  }
+}
+
 // Runs the whole pipeline with ONE host synchronisation: H2D (host inputs),
 // K1, K2, K3, the cooperative round kernel, K5 (device outputs), and the
 // read-back of the control block + the first STATS_EAGER round stats.
@@ -305,9 +364,9 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
     double* sy = (double*)((char*)ws.stage + align_up(8 * ws.n_cap, 256));
     uint32_t* sid = (uint32_t*)((char*)ws.stage + 2 * align_up(8 * ws.n_cap, 256));
     const cudaMemcpyKind k = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-    CK(cudaMemcpyAsync(sx, rq.x, 8 * n, k, st));
-    CK(cudaMemcpyAsync(sy, rq.y, 8 * n, k, st));
-    if (rq.ids) CK(cudaMemcpyAsync(sid, rq.ids, 4 * n, k, st));
+    h2d_or_copy(sx, rq.x, 8 * n, k, host, st);
+    h2d_or_copy(sy, rq.y, 8 * n, k, host, st);
+    if (rq.ids) h2d_or_copy(sid, rq.ids, 4 * n, k, host, st);
     B.in_x = sx;
     B.in_y = sy;
     B.in_id = rq.ids ? sid : nullptr;
