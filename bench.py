@@ -326,7 +326,10 @@ def run_b200(a):
             m = hull.run_device(mx, my, a.mode, ids=mids, stream=sp, stats=False)
             launches[0] += m.kernel_launches
             return m
-        return shardmod.merged_hull(dh, first, world, all_gather, hull_with_ids)
+        m = shardmod.merged_hull(dh, first, world, all_gather, hull_with_ids)
+        if os.environ.get("SHB_BENCH_DEBUG"):
+            print(f"[rank {rank}] shard h {dh.h} first {first} merged h {m.h}", file=sys.stderr, flush=True)
+        return m
 
     def max_over_ranks(v):
         t = torch.tensor([v], dtype=torch.float64, device="cpu" if share else dev)

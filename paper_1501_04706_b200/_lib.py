@@ -81,14 +81,29 @@ def load() -> ctypes.CDLL:
     L.sh_b200_gen_circle_host.argtypes = [_vp, _vp, _u64, _u64]
     L.sh_b200_device_info.argtypes = [ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_char_p,
                                       ctypes.c_size_t]
-    L.sh_b200_read_pts2.argtypes = [ctypes.c_char_p, ctypes.c_int, _vp, _vp, _vp, _u64, _vp,
-                                    ctypes.c_char_p, ctypes.c_size_t]
-    L.sh_b200_read_pts2.restype = ctypes.c_int
-    L.sh_b200_preprocess.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp, _vp, _vp, _u64, _vp, _vp,
-                                     ctypes.c_char_p, ctypes.c_size_t]
-    L.sh_b200_preprocess.restype = ctypes.c_int
+    if hasattr(L, "sh_b200_read_pts2"):  # (absent from older builds used in A/B runs)
+        L.sh_b200_read_pts2.argtypes = [ctypes.c_char_p, ctypes.c_int, _vp, _vp, _vp, _u64, _vp,
+                                        ctypes.c_char_p, ctypes.c_size_t]
+        L.sh_b200_read_pts2.restype = ctypes.c_int
+    if hasattr(L, "sh_b200_preprocess"):
+        L.sh_b200_preprocess.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp, _vp, _vp, _u64, _vp,
+                                         _vp, ctypes.c_char_p, ctypes.c_size_t]
+        L.sh_b200_preprocess.restype = ctypes.c_int
     L.sh_b200_release_pool.argtypes = []
     L.sh_b200_release_pool.restype = None
     L.sh_b200_abi_version.restype = ctypes.c_int
     _lib = L
     return L
+
+
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the (synchronising) legacy default stream
+
+
+def stream_handle(s):
+    """A torch stream's cuda_stream as the C-ABI's stream argument.  torch's
+    default stream reports 0, which the C-ABI reads as "use the library's own
+    (non-blocking) stream" -- work queued by torch before the call would then
+    not be ordered before the hull.  Map it to cudaStreamLegacy instead."""
+    if s is None:
+        return None
+    return CUDA_STREAM_LEGACY if int(s) == 0 else int(s)

@@ -78,7 +78,8 @@ def gen_uniform_device(n: int, seed: int, first: int = 0, device: int = 0, strea
     y = torch.empty(n, dtype=torch.float64, device=dev)
     if stream is None:
         stream = torch.cuda.current_stream(dev).cuda_stream
-    rc = L.sh_b200_gen_uniform(x.data_ptr(), y.data_ptr(), first, n, seed, device, stream)
+    rc = L.sh_b200_gen_uniform(x.data_ptr(), y.data_ptr(), first, n, seed, device,
+                               _lib.stream_handle(stream))
     if rc:
         raise RuntimeError(f"sh_b200_gen_uniform failed ({rc})")
     return x, y
@@ -92,7 +93,7 @@ def gen_disk_device(n: int, seed: int, device: int = 0, stream=None):
     y = torch.empty(n, dtype=torch.float64, device=dev)
     if stream is None:
         stream = torch.cuda.current_stream(dev).cuda_stream
-    rc = L.sh_b200_gen_disk(x.data_ptr(), y.data_ptr(), n, seed, device, stream)
+    rc = L.sh_b200_gen_disk(x.data_ptr(), y.data_ptr(), n, seed, device, _lib.stream_handle(stream))
     if rc:
         raise RuntimeError(f"sh_b200_gen_disk failed ({rc})")
     return x, y
@@ -148,7 +149,7 @@ def read_points_binary_device(path, device: int = 0, stream=None):
     y = torch.empty(n.value, dtype=torch.float64, device=dev)
     if stream is None:
         stream = torch.cuda.current_stream(dev).cuda_stream
-    rc = L.sh_b200_read_pts2(p, device, stream, x.data_ptr(), y.data_ptr(), n.value,
+    rc = L.sh_b200_read_pts2(p, device, _lib.stream_handle(stream), x.data_ptr(), y.data_ptr(), n.value,
                              ctypes.byref(n), err, 512)
     if rc:
         _raise(rc, err.value.decode(errors="replace"))

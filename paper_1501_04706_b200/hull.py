@@ -270,7 +270,7 @@ def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, st
     req.mode = int(mode)
     req.flags = flags
     req.device = int(device)
-    req.stream = stream
+    req.stream = _lib.stream_handle(stream)
     st = _stats_buffer(stats_cap)
     res.idx = oi
     res.x = ox
@@ -305,6 +305,9 @@ def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int |
     x, y, ids, px, py, dx, n = _prepare(x, y, ids)
     if device is None:
         device = int(x.device.index) if dx else 0
+    if dx and stream is None:  # order the hull after torch's queued work on these tensors
+        import torch
+        stream = torch.cuda.current_stream(x.device).cuda_stream
     capacity = max(int(cap if cap is not None else max(n, 2)), 2)
     ox = np.empty(capacity, np.float64)
     oy = np.empty(capacity, np.float64)
@@ -382,7 +385,8 @@ def preprocess_device(x, y, *, stream: int | None = None):
     oy = torch.empty(max(n, 1), dtype=torch.float64, device=x.device)
     kept, disc = ctypes.c_uint64(0), ctypes.c_uint64(0)
     err = ctypes.create_string_buffer(256)
-    rc = L.sh_b200_preprocess(px, py, n, device, stream, ox.data_ptr(), oy.data_ptr(), n,
+    rc = L.sh_b200_preprocess(px, py, n, device, _lib.stream_handle(stream), ox.data_ptr(),
+                              oy.data_ptr(), n,
                               ctypes.byref(kept), ctypes.byref(disc), err, 256)
     if rc:
         _raise(rc, err.value.decode(errors="replace"))

@@ -43,8 +43,12 @@ def _oracle_hull(x, y, mode):
 
 def _oracle_hull_ids(mx, my, mids, mode):
     """The C-ABI's ids rule restated for the test: the hull of the gathered
-    points, each vertex reported with the lowest id among equal coordinates."""
-    x, y, ids = mx.numpy(), my.numpy(), mids.numpy().astype(np.int64)
+    points, each vertex reported with the lowest id among equal coordinates.
+    Non-finite input raises hull.Error(NonFiniteInput), like the C-ABI."""
+    from paper_1501_04706_b200 import hull
+    x, y, ids = mx.numpy(), my.numpy(), mids.numpy().astype(np.int64) & 0xFFFFFFFF
+    if not (np.isfinite(x).all() and np.isfinite(y).all()):
+        raise hull.Error(hull.Errc.NonFiniteInput, "non-finite input")
     hx, hy, _ = _oracle_hull(x, y, mode)
     out = []
     for a, b in zip(hx, hy):
@@ -52,7 +56,7 @@ def _oracle_hull_ids(mx, my, mids, mode):
     return _Hull(hx, hy, np.array(out, np.int64))
 
 
-def _worker(rank, world, port, x, y, mode, q):
+def _worker(rank, world, port, x, y, mode, q, hmax=shard.HMAX):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -61,7 +65,8 @@ def _worker(rank, world, port, x, y, mode, q):
             first, cnt = shard.shard_range(x.size, world, rank)
             lx, ly, li = _oracle_hull(x[first:first + cnt], y[first:first + cnt], mode)
             m = shard.merged_hull(_Hull(lx, ly, li), first, world, dist.all_gather_into_tensor,
-                                  lambda mx, my, mids: _oracle_hull_ids(mx, my, mids, mode))
+                                  lambda mx, my, mids: _oracle_hull_ids(mx, my, mids, mode),
+                                  hmax=hmax)
             q.put((rank, m.x.numpy().copy(), m.y.numpy().copy(), m.indices.numpy().copy()))
         finally:
             dist.destroy_process_group()
@@ -69,14 +74,15 @@ def _worker(rank, world, port, x, y, mode, q):
         q.put((rank, "error", repr(e), None))
 
 
-def _run(x, y, mode, world=2):
+def _run(x, y, mode, world=2, hmax=shard.HMAX):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     os.environ["PYTHONPATH"] = os.pathsep.join(
         [root, os.path.join(root, "tests"), os.environ.get("PYTHONPATH", "")])
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, x, y, mode, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, x, y, mode, q, hmax))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
@@ -98,6 +104,16 @@ def test_shard_merge_equals_full_hull(mode):
         assert np.array_equal(hx.view(np.uint64), ref.x.view(np.uint64)), rank
         assert np.array_equal(hy.view(np.uint64), ref.y.view(np.uint64)), rank
         assert np.array_equal(hi, ref_idx), rank
+
+
+def test_shard_merge_fixed_gather_overflow_falls_back():
+    """Shard hulls larger than the fixed gather (hmax) send NaN payloads; the
+    merge then redoes the gather with exact sizes -- same result."""
+    x, y = dataio.gen_circle(2_000, 3)  # every point is a hull vertex
+    ref = oracle.hull_run(x, y, 1)
+    for rank, hx, hy, hi in _run(x, y, 1, hmax=64):
+        assert np.array_equal(hx.view(np.uint64), ref.x.view(np.uint64)), rank
+        assert np.array_equal(hi, oracle.canonical_index(x, y, ref.x, ref.y)), rank
 
 
 def test_shard_merge_duplicates_across_ranks():
