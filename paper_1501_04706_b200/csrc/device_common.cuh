@@ -510,7 +510,7 @@ struct TileRing {
   }
   // thread 0: stream points [first, first + cnt) into stage s
   SH_DEV void issue(int s, const double* X, const double* Y, const uint32_t* I, uint32_t first,
-                    uint32_t cnt, const unsigned char* A = nullptr) {
+                    uint32_t cnt, const unsigned char* A = nullptr, bool with_aux = true) {
     const uint32_t c4 = cnt & ~3u;
     const uint32_t ab = AUX ? ((cnt + 63) / 64) * AUX : 0u;
     if (c4 == 0 && ab == 0) {  // nothing to copy: complete the phase with a plain arrival
@@ -525,6 +525,11 @@ struct TileRing {
       tma_load_1d(ys + s * T, Y + first, c4 * 8u, bar + s);
       if (IDS) tma_load_1d(is + s * T, I + first, c4 * 4u, bar + s);
     }
+    if (ab && with_aux) tma_load_1d(aux + s * kAuxBytes, A + (size_t)(first / 64) * AUX, ab, bar + s);
+  }
+  // the aux bytes of a stage whose point bytes (and expected count) were issued
+  SH_DEV void issue_aux(int s, uint32_t first, uint32_t cnt, const unsigned char* A) {
+    const uint32_t ab = AUX ? ((cnt + 63) / 64) * AUX : 0u;
     if (ab) tma_load_1d(aux + s * kAuxBytes, A + (size_t)(first / 64) * AUX, ab, bar + s);
   }
   SH_DEV void wait(int s, uint32_t parity) { mbar_wait(bar + s, parity); }
@@ -539,30 +544,89 @@ struct TileRing {
 
 namespace shb {
 
+// The tiles this CTA streams: b, b+G, ... (mapped to ntiles-1-t when `reverse`).
+template <int T>
+struct TileWalk {
+  uint32_t ntiles, mine;
+  bool reverse;
+  SH_DEV TileWalk(uint32_t n, bool rev) : reverse(rev) {
+    ntiles = (n + T - 1) / T;
+    mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  }
+  SH_DEV uint32_t first(uint32_t k) const {
+    const uint32_t t = blockIdx.x + k * gridDim.x;
+    return (reverse ? ntiles - 1 - t : t) * T;
+  }
+};
+
+// Producer lane, before the kernel's griddepcontrol.wait: start the ring on
+// the first min(NS, mine) tiles of inputs that do not depend on the previous
+// kernel (the point arrays; with_aux = false leaves out the aux bytes, which
+// stream_input issues for these stages once the wait returned).  Returns the
+// number of tiles started; every thread computes the same value.
+template <int T, int NS, bool IDS, int AUX, int NCW>
+SH_DEV uint32_t stream_prefetch(TileRing<T, NS, IDS, AUX, NCW>& R, uint32_t n, const double* X,
+                                const double* Y, const uint32_t* I, bool reverse, bool with_aux) {
+  const TileWalk<T> w(n, reverse);
+  const uint32_t pre = min(w.mine, (uint32_t)NS);
+  if ((int)(threadIdx.x >> 5) == NCW && (threadIdx.x & 31) == 0) {
+    for (uint32_t k = 0; k < pre; ++k) {
+      const uint32_t first = w.first(k);
+      R.issue((int)k, X, Y, I, first, min((uint32_t)T, n - first), nullptr, with_aux);
+    }
+  }
+  return pre;
+}
+
+// A CTA that started tiles but leaves early waits for their bulk copies.
+template <int T, int NS, bool IDS, int AUX, int NCW>
+SH_DEV void stream_drain(TileRing<T, NS, IDS, AUX, NCW>& R, uint32_t pre) {
+  if (threadIdx.x == 0)
+    for (uint32_t k = 0; k < pre; ++k) R.wait((int)k, 0u);
+  __syncthreads();
+}
+
+// As stream_drain, for stages prefetched without their aux bytes: those are
+// issued first (the stage's expected byte count includes them).
+template <int T, int NS, bool IDS, int AUX, int NCW>
+SH_DEV void stream_drain_points(TileRing<T, NS, IDS, AUX, NCW>& R, uint32_t pre, uint32_t n,
+                                const unsigned char* A) {
+  const TileWalk<T> w(n, false);
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < pre; ++k) {
+      const uint32_t first = w.first(k);
+      R.issue_aux((int)k, first, min((uint32_t)T, n - first), A);
+    }
+    for (uint32_t k = 0; k < pre; ++k) R.wait((int)k, 0u);
+  }
+  __syncthreads();
+}
+
 // Streams this CTA's share of the input through the ring: tiles b, b+G, ...
 // (mapped to ntiles-1-t when `reverse`), calling body(stage, first, cnt) in
 // the NCW consumer warps for each tile after its bytes landed.  Warp
 // NCW is a dedicated producer: it refills a stage as soon as every
 // consumer warp released it (empty mbarrier), so no consumer ever waits for
-// another consumer and no CTA-wide barrier is needed per tile.  The caller
-// initialised the ring (+ __syncthreads); a __syncthreads ends the stream.
+// another consumer and no CTA-wide barrier is needed per tile.  `pre` tiles
+// were already started by stream_prefetch (without their aux bytes when
+// aux_pending).  The caller initialised the ring (+ __syncthreads); a
+// __syncthreads ends the stream.
 template <int T, int NS, bool IDS, int AUX, int NCW, class Body>
 SH_DEV void stream_input(TileRing<T, NS, IDS, AUX, NCW>& R, uint32_t n, const double* X,
                          const double* Y, const uint32_t* I, const unsigned char* A, bool reverse,
-                         const Body& body) {
-  const uint32_t ntiles = (n + T - 1) / T;
-  const uint32_t G = gridDim.x, b = blockIdx.x;
-  const uint32_t mine = b < ntiles ? (ntiles - 1 - b) / G + 1 : 0;
-  auto tile_of = [&](uint32_t k) {
-    const uint32_t t = b + k * G;
-    return reverse ? ntiles - 1 - t : t;
-  };
+                         const Body& body, uint32_t pre = 0, bool aux_pending = false) {
+  const TileWalk<T> w(n, reverse);
+  const uint32_t mine = w.mine;
   if ((int)(threadIdx.x >> 5) == NCW) {  // producer warp
     if ((threadIdx.x & 31) == 0) {
-      for (uint32_t k = 0; k < mine; ++k) {
+      for (uint32_t k = 0; k < pre && aux_pending; ++k) {
+        const uint32_t first = w.first(k);
+        R.issue_aux((int)k, first, min((uint32_t)T, n - first), A);
+      }
+      for (uint32_t k = pre; k < mine; ++k) {
         const int s = (int)(k % NS);
         if (k >= (uint32_t)NS) mbar_wait(R.ebar + s, ((k / NS) - 1) & 1u);
-        const uint32_t first = tile_of(k) * T;
+        const uint32_t first = w.first(k);
         R.issue(s, X, Y, I, first, min((uint32_t)T, n - first), A);
       }
     }
@@ -570,7 +634,7 @@ SH_DEV void stream_input(TileRing<T, NS, IDS, AUX, NCW>& R, uint32_t n, const do
     for (uint32_t k = 0; k < mine; ++k) {
       const int s = (int)(k % NS);
       R.wait(s, (k / NS) & 1u);
-      const uint32_t first = tile_of(k) * T;
+      const uint32_t first = w.first(k);
       body(s, first, min((uint32_t)T, n - first));
       R.release(s);
     }

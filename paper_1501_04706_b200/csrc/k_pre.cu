@@ -335,13 +335,29 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   TileRing<Cfg2::T, Cfg2::NS, IDS, 0, Cfg2::CW> R;
   R.carve(smem_raw);
   Ctl* c = B.ctl;
+#ifndef SHB_K2_REVERSE
+#define SHB_K2_REVERSE 1
+#endif
+  // CTA-wide running maxima of the two chains' distances (positive doubles
+  // order like their bits): a point below them cannot be the CTA's farthest,
+  // so the per-point candidate branch is almost never taken
+  __shared__ unsigned long long s_dmax[2];
+  if (threadIdx.x == 0) {
+    R.init();
+    s_dmax[0] = s_dmax[1] = 0ull;
+  }
+  __syncthreads();
+  // the points do not depend on K1: start the ring before waiting for it
+  const uint32_t pre = stream_prefetch(R, B.n, B.in_x, B.in_y, B.in_id, SHB_K2_REVERSE != 0, true);
   pdl_wait();               // K1's partial extremes are complete and visible
   pdl_launch_dependents();  // K3 may be scheduled on SMs this kernel frees
-  if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   // ---- every CTA combines K1's per-CTA extremes (no serial last-CTA step) ----
   __shared__ Fin s_fin;
   combine_k1(B, s_fin, true);
-  if (s_fin.status != ST_RUNNING) return;
+  if (s_fin.status != ST_RUNNING) {
+    stream_drain(R, pre);
+    return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n = B.n;
   const double* __restrict__ X = B.in_x;
@@ -364,15 +380,6 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   Cand a0 = empty_cand(), a1 = empty_cand();
   uint32_t kept = 0;
   bool noncol = false;
-  // CTA-wide running maxima of the two chains' distances (positive doubles
-  // order like their bits): a point below them cannot be the CTA's farthest,
-  // so the per-point candidate branch is almost never taken
-  __shared__ unsigned long long s_dmax[2];
-  if (threadIdx.x == 0) {
-    R.init();
-    s_dmax[0] = s_dmax[1] = 0ull;
-  }
-  __syncthreads();
 
   // With 4 distinct corners, edge q starts at corner q (left, bottom, right,
   // top) and the chain base lines start at left (P0) and right (Pr), so the
@@ -388,9 +395,6 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   // backwards over the input: K1 just left the tail in L2, K3 starts at the head
   constexpr int NCH = Cfg2::T / 64 / Cfg2::CW;  // chunks per consumer warp per tile
   constexpr int NP = 2 * NCH;                  // points per thread per tile
-#ifndef SHB_K2_REVERSE
-#define SHB_K2_REVERSE 1
-#endif
   // One tile; FULLT: cnt == T (no bounds checks anywhere).  All decisions are
   // bitwise predicates; the rare candidate updates sit behind one
   // warp-uniform branch.
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
         tile(std::true_type{}, qk, s, first, cnt);
       else
         tile(std::false_type{}, qk, s, first, cnt);
-    });
+    }, pre);
   };
   if (quad4)
     pass(std::integral_constant<int, 1>{});

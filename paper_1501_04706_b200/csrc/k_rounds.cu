@@ -257,9 +257,17 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   __shared__ uint32_t s_ws[MAXW + 1];
   __shared__ int s_last;
   Ctl* c = B.ctl;
+  if (threadIdx.x == 0) R.init();
+  __syncthreads();
+  // the points do not depend on K2 (their class bits do): start the ring on
+  // them before waiting; the bits follow once K2 is complete
+  const uint32_t pre = stream_prefetch(R, B.n, B.in_x, B.in_y, B.in_id, false, false);
   pdl_wait();               // K2's classes and partials are complete and visible
   pdl_launch_dependents();  // the round kernel may be scheduled on SMs this kernel frees
-  if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
+  if (*(volatile uint32_t*)&c->status != ST_RUNNING) {
+    stream_drain_points(R, pre, B.n, reinterpret_cast<const unsigned char*>(B.bits));
+    return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n = B.n;
   const double* __restrict__ X = B.in_x;
@@ -336,12 +344,14 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
       }
     }
     __syncthreads();
-    if (s_status != ST_RUNNING) return;
+    if (s_status != ST_RUNNING) {
+      stream_drain_points(R, pre, B.n, reinterpret_cast<const unsigned char*>(B.bits));
+      return;
+    }
   }
 
   // ---- table phase (S = 2: the lower chain P0->Pr and the upper chain Pr->P0) ----
   if (threadIdx.x == 0) {
-    R.init();
     uint32_t ns = 0, Slon = 1;
     const double hx[2] = {__ldcg(&c->ext_x[0]), __ldcg(&c->ext_x[2])};
     const double hy[2] = {__ldcg(&c->ext_y[0]), __ldcg(&c->ext_y[2])};
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
       tile(std::true_type{}, s, first, cnt);
     else
       tile(std::false_type{}, s, first, cnt);
-  });
+  }, pre, true);
   if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[512 + blockIdx.x] = globaltimer_ns() - c->t0_ns;
 
   // ---- flush the CTA's records to the global slots of round 2's argmax ----
