@@ -280,15 +280,6 @@ SH_DEV void rec_update(SlotRec* rec, const Cand& c, bool lower) {
   }
 }
 
-// global slot offer (the record is read by other CTAs / the next round)
-SH_DEV void rec_offer(unsigned long long* dbits, SlotRec* rec, const Cand& c, bool lower) {
-  const unsigned long long mine = (unsigned long long)__double_as_longlong(c.d);
-  if (mine < *(volatile unsigned long long*)dbits) return;
-  const unsigned long long old = atomicMax(dbits, mine);
-  if (mine < old) return;
-  rec_update<false>(rec, c, lower);
-}
-
 // relaxed gpu-scope atomic add issued from one lane: inline PTX so the
 // compiler cannot turn it into a warp-aggregated atomic whose result is
 // shuffled (and therefore waited for) right away

@@ -4,20 +4,23 @@
 //   K3 k3_round1  round 1 straight from the input + K2's class bits: route
 //                 every member of the two chains to the A->C or C->B edge of
 //                 its chain's farthest point C, keep iff strictly outside
-//                 (hull.cpp:196-201), compact the survivors into the live set
-//                 and fuse the farthest-point search of round 2
+//                 (hull.cpp:196-201), append the survivors to the CTA's run
+//                 of the live set and find round 2's farthest points
 //   KR k_rounds   every later round in ONE persistent cooperative launch:
-//                 per round a segment-table phase (rebuilt redundantly in each
-//                 CTA's shared memory for small tables, a grid-wide scan for
-//                 large ones), a point phase (route, keep, compact, offer) and
-//                 one grid barrier; once the live set is small, CTA 0 finishes
-//                 the remaining rounds alone with __syncthreads only
+//                 per round a segment-table phase (rebuilt in each CTA's
+//                 shared memory for small tables, a grid-wide scan for large
+//                 ones), a point phase (route, keep, append, contend) and grid
+//                 barriers; once a lone CTA holds a small table and a live set
+//                 that fits on chip, it finishes in shared memory (solo tail)
 //   K5 k5_emit    copy the final heads (the hull, CCW from P0) to the caller
 //
 // Compaction is order-free: the hull and the per-round stats depend only on
 // segment membership and on the total order of the farthest-point
-// comparator, never on where a survivor lands, so every tile reserves its
-// output range with ONE atomicAdd and no scan/look-back is needed.
+// comparator, never on where a survivor lands.  Each CTA appends to its own
+// run with one shared-memory atomicAdd per warp; the next round reads the
+// runs as one virtual range.  Farthest points between CTAs: per-CTA record
+// rows or contender lists plus atomicMax on the distance bits, winners
+// claimed by compare-and-swap after the barrier -- no global locks.
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -30,16 +33,6 @@ namespace shb {
 // ===========================================================================
 // shared pieces
 // ===========================================================================
-
-SH_DEV Route ldcg_route(const Route* p) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-  const double2 a = __ldcg(q), b = __ldcg(q + 1), cc = __ldcg(q + 2);
-  const uint4 t = __ldcg(reinterpret_cast<const uint4*>(q + 3));
-  Route r;
-  r.ax = a.x; r.ay = a.y; r.cx = b.x; r.cy = b.y; r.bx = cc.x; r.by = cc.y;
-  r.cid = t.x; r.ns = t.y; r.flags = t.z; r.pad = t.w;
-  return r;
-}
 
 // Route one member (x, y, id) of old segment s whose Route row is at rp
 // (shared or, with GLOBAL, global memory), SURVEY.md section 7.3:
@@ -162,19 +155,6 @@ SH_DEV void contend_tile(unsigned long long* s_db, SlotRec* s_rec, uint32_t keep
           rec_update<true>(&s_rec[pseg[j]], me, (lowm >> j) & 1u);
         }
       }
-    }
-  }
-}
-
-// CTA records -> global records of the next round's farthest points
-SH_DEV void flush_slots(const unsigned long long* s_db, const SlotRec* s_rec, uint32_t Sn,
-                        uint32_t Slon, unsigned long long* Sd, SlotRec* Srec) {
-  for (uint32_t t = threadIdx.x; t < Sn; t += blockDim.x) {
-    const volatile SlotRec* r = s_rec + t;
-    if (r->id != NONE) {
-      Cand me;
-      me.d = r->d; me.x = r->x; me.y = r->y; me.id = r->id; me.pos = 0;
-      rec_offer(Sd + t, Srec + t, me, t < Slon);
     }
   }
 }
