@@ -325,21 +325,39 @@ def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int |
     return r
 
 
-@dataclass
 class DeviceHull:
-    """A hull whose vertices stay in HBM (SH_OUT_DEVICE): torch CUDA tensors."""
-    x: object
-    y: object
-    indices: object
-    h: int
-    stats: list
-    phase_timings: PhaseTimings
-    kernels: KernelTimings
-    kept: int
-    rounds: int
-    kernel_launches: int
-    round_end_ms: list = field(default_factory=list)
-    round_phases_ms: list = field(default_factory=list)
+    """A hull whose vertices stay in HBM (SH_OUT_DEVICE): torch CUDA tensors.
+    x, y, indices are views of the output buffers, created on first access
+    (slicing three tensors costs more host time than the rest of the wrapper)."""
+    __slots__ = ("_bufs", "_views", "h", "stats", "phase_timings", "kernels", "kept", "rounds",
+                 "kernel_launches", "round_end_ms", "round_phases_ms")
+
+    def __init__(self, x, y, indices, h: int, stats, phase_timings, kernels, kept: int,
+                 rounds: int, kernel_launches: int, round_end_ms=(), round_phases_ms=()):
+        self._bufs = (x, y, indices)  # full buffers (or already the views)
+        self._views = None
+        self.h = h
+        self.stats = stats
+        self.phase_timings = phase_timings
+        self.kernels = kernels
+        self.kept = kept
+        self.rounds = rounds
+        self.kernel_launches = kernel_launches
+        self.round_end_ms = round_end_ms
+        self.round_phases_ms = round_phases_ms
+
+    def _v(self, i):
+        if self._views is None:
+            self._views = tuple(b[:self.h] for b in self._bufs)
+        return self._views[i]
+
+    x = property(lambda self: self._v(0))
+    y = property(lambda self: self._v(1))
+    indices = property(lambda self: self._v(2))
+
+    def __repr__(self) -> str:
+        return (f"DeviceHull(h={self.h}, rounds={self.rounds}, kept={self.kept}, "
+                f"kernel_launches={self.kernel_launches})")
 
 
 def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int | None = None,
@@ -365,7 +383,7 @@ def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int |
                              device, stream, ox.data_ptr(), oy.data_ptr(), oi.data_ptr(),
                              int(ox.shape[0]), (1 << 16) if stats else 0)
     h = int(res.h)
-    return DeviceHull(ox[:h], oy[:h], oi[:h], h, sts, ph, kt, int(res.kept), int(res.rounds),
+    return DeviceHull(ox, oy, oi, h, sts, ph, kt, int(res.kept), int(res.rounds),
                       int(res.kernel_launches), ends[0], ends[1])
 
 
