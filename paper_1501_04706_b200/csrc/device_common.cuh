@@ -329,6 +329,22 @@ SH_DEV void grid_barrier(uint32_t* count, uint32_t* gen, uint32_t nblocks) {
   __syncthreads();
 }
 
+// Grid barrier on a monotone arrival counter: each participating CTA adds 1
+// (release) and waits until the counter reaches `target` (acquire), the
+// running total of participants over all barriers so far -- the last arrival
+// completes the barrier itself, with no reset and no second word to publish.
+SH_DEV void grid_barrier_ctr(unsigned long long* ctr, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // Decoupled look-back (single-pass device-wide exclusive scan of per-tile
 // counts).  Status words pack (epoch:30 | flag:2) << 32 | value:32; a word

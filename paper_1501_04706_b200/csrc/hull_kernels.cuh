@@ -198,6 +198,7 @@ struct __align__(16) Ctl {
   unsigned long long t0_ns;  // %globaltimer when K1 started (per-round timestamps)
   unsigned long long mark[8]; // device times (ns since t0): K1 end, K2 start/end, K3 start/end, KR start/end
   unsigned long long tl[32]; // debug timeline of CTA 0 (sh_b200_last_timeline)
+  unsigned long long bar_ctr; // round kernel: arrivals at its grid barriers (never reset in a call)
   uint32_t tl_round;         // round whose tiles are traced (0: none)
   uint32_t tl_n;
 };

@@ -552,8 +552,20 @@ struct RoundSmem {
 };
 
 // Barrier over the CTAs still working on the rounds.
-SH_DEV void rounds_barrier(Ctl* c, uint32_t P) {
+#ifndef SHB_BAR_CTR
+#define SHB_BAR_CTR 1
+#endif
+// `bar` is this CTA's running arrival target (the same on every participant)
+SH_DEV void rounds_barrier(Ctl* c, uint32_t P, unsigned long long& bar) {
+#if SHB_BAR_CTR
+  if (P > 1) {
+    bar += P;
+    grid_barrier_ctr(&c->bar_ctr, bar);
+    return;
+  }
+#else
   if (P > 1) grid_barrier(&c->bar_count, &c->bar_gen, P);
+#endif
   else __syncthreads();
 }
 
@@ -664,7 +676,7 @@ constexpr int TS = SHB_TS;
 
 SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, uint32_t pout,
                         uint32_t sin, uint32_t sout, uint32_t P, bool from_rec, const RecSrc& rs,
-                        uint32_t* s_ws, uint32_t& Sn, uint32_t& Slon) {
+                        uint32_t* s_ws, uint32_t& Sn, uint32_t& Slon, unsigned long long& bar) {
   Ctl* c = B.ctl;
   constexpr uint32_t STEP = RTPB * TS;
   // CTA ranges are whole warp chunks (32 * TS), so that the lane mapping is
@@ -701,7 +713,7 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
       B.blk_cnt[MAX_ROUND_BLOCKS + blockIdx.x] = t2;
     }
   }
-  rounds_barrier(c, P);
+  rounds_barrier(c, P, bar);
   // T2: prefix of this CTA + totals
   uint32_t pre = 0, tot = 0, tot_lo = 0;
   for (uint32_t b = threadIdx.x; b < P; b += RTPB) {
@@ -821,7 +833,7 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
     }
     running += total;
   }
-  rounds_barrier(c, P);
+  rounds_barrier(c, P, bar);
   return true;
 }
 
@@ -1067,6 +1079,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   const uint32_t target = min(ROUND_TARGET, q);
   uint32_t P = gridDim.x;
   uint32_t rec_kind = RS_SREC;  // where this round's input records are (RecSrc)
+  unsigned long long bar = 0;   // grid-barrier arrival target (rounds_barrier)
   auto rec_src = [&](uint32_t kind, uint32_t rr) {
     RecSrc rs;
     rs.kind = kind;
@@ -1120,7 +1133,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     if (small) {
       table_small(B, sm, S, Slo, pin, pout, rec_src(rec_kind, r), s_ws, Sn, Slon);
     } else if (!table_large(B, S, Slo, pin, pout, sin, sout, P, prev_small, rec_src(rec_kind, r),
-                            s_ws, Sn, Slon)) {
+                            s_ws, Sn, Slon, bar)) {
       return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) t_table = globaltimer_ns();
@@ -1303,11 +1316,11 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     if (blockIdx.x == 0 && threadIdx.x == 0) t_points = globaltimer_ns();
     if (threadIdx.x == 0 && r == trace_r) B.dbg[blockIdx.x] = globaltimer_ns() - c->t0_ns;
     KR_MARK();  // slots flushed
-    rounds_barrier(c, P);
+    rounds_barrier(c, P, bar);
     KR_MARK();  // barrier passed
     if (small && !keep_smem) {  // rows at the final maxima claim their slots
       claim_slots(sm.rec, Sn, Slon, Sd, B.Wn[sout], B.Rc[r & 1u]);
-      rounds_barrier(c, P);
+      rounds_barrier(c, P, bar);
     }
     if (!small) {
       // winner pass over this CTA's contenders (listed in its run's slice of
@@ -1355,7 +1368,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
           }
         }
       }
-      rounds_barrier(c, P);
+      rounds_barrier(c, P, bar);
     }
 
     KR_MARK();  // winner pass done
