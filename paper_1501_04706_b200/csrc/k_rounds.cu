@@ -670,7 +670,7 @@ SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, 
 // slots / distance maxima of their children.  Returns false on segment-table
 // overflow (every CTA returns consistently).
 #ifndef SHB_TS
-#define SHB_TS 8
+#define SHB_TS 4
 #endif
 constexpr int TS = SHB_TS;
 
@@ -742,26 +742,18 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   unsigned long long* Sdo = B.Sd[sout];
   const uint32_t lt = lanemask_lt();
   uint32_t running = pre_all;
-  // every step covers [lo + k*STEP, lo + (k+1)*STEP): warps in order
+  // every step covers [lo + k*STEP, lo + (k+1)*STEP): warps in order.  All
+  // loads of a step -- the heads, and for split segments the next head and C
+  // -- are issued before the step's block scan, so one memory round trip
+  // overlaps the scan; the end point B of segment s is the head of s + 1,
+  // taken from the neighbouring lane.
   for (uint32_t b0 = lo; b0 < hi; b0 += STEP) {
     const uint32_t g0 = b0 + wid * 32 * TS;
     uint32_t w[TS];
 #pragma unroll
     for (int i = 0; i < TS; ++i) w[i] = split_of(g0 + i * 32 + lane);
-    uint32_t wpre[TS], wtot = 0;
-#pragma unroll
-    for (int i = 0; i < TS; ++i) {
-      const uint32_t bal = __ballot_sync(FULL, w[i] != NONE);
-      wpre[i] = wtot + __popc(bal & lt);
-      wtot += __popc(bal);
-    }
-    uint32_t total;
-    const uint32_t wx = block_exclusive_scan(lane == 0 ? wtot : 0u, s_ws, &total);
-    const uint32_t wbase = running + __shfl_sync(FULL, wx, 0);
-    // all loads of the step first (independent, in flight together), then
-    // the stores
-    double ax[TS], ay[TS];
-    uint32_t aid[TS];
+    double ax[TS], ay[TS], cx[TS], cy[TS];
+    uint32_t aid[TS], cid[TS];
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
       const uint32_t s = min(g0 + i * 32 + lane, S - 1);
@@ -771,30 +763,11 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
     }
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
-      const uint32_t s = g0 + i * 32 + lane;
-      if (s < hi) {
-        const uint32_t ns = s + wbase + wpre[i];
-        Ox[ns] = ax[i];
-        Oy[ns] = ay[i];
-        Oid[ns] = aid[i];
-        Wout[ns] = NONE;
-      }
-    }
-    // split segments: route row + head C + the children's slots (loads of
-    // the whole step first again)
-    double bx[TS], by[TS], cx[TS], cy[TS];
-    uint32_t cid[TS];
-#pragma unroll
-    for (int i = 0; i < TS; ++i) {
-      const uint32_t s = g0 + i * 32 + lane;
-      bx[i] = by[i] = cx[i] = cy[i] = 0.0;
+      cx[i] = cy[i] = 0.0;
       cid[i] = NONE;
-      if (s < hi && w[i] != NONE) {
-        const uint32_t sb = s + 1 == S ? 0u : s + 1;
-        bx[i] = __ldcg(Tx + sb);
-        by[i] = __ldcg(Ty + sb);
+      if (w[i] != NONE) {  // implies s < hi
         if (from_rec) {
-          const SlotRec* cr = rec_at(rs, s);  // global (RS_SREC or RS_ROWS), a winner exists
+          const SlotRec* cr = rec_at(rs, g0 + i * 32 + lane);  // global, a winner exists
           cx[i] = __ldcg(&cr->x);
           cy[i] = __ldcg(&cr->y);
           cid[i] = __ldcg(&cr->id);
@@ -806,29 +779,59 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
         }
       }
     }
+    uint32_t wpre[TS], wtot = 0;
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      const uint32_t bal = __ballot_sync(FULL, w[i] != NONE);
+      wpre[i] = wtot + __popc(bal & lt);
+      wtot += __popc(bal);
+    }
+    uint32_t total;
+    const uint32_t wx = block_exclusive_scan(lane == 0 ? wtot : 0u, s_ws, &total);
+    const uint32_t wbase = running + __shfl_sync(FULL, wx, 0);
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
       const uint32_t s = g0 + i * 32 + lane;
-      if (s < hi && w[i] != NONE) {
+      // B = head of s + 1: lane + 1 of this row, lane 0 of the next row, or
+      // (last lane of the last row, the table's last segment) a load
+      double bx = __shfl_down_sync(FULL, ax[i], 1);
+      double by = __shfl_down_sync(FULL, ay[i], 1);
+      if (i + 1 < TS) {
+        const double nx = __shfl_sync(FULL, ax[i + 1 < TS ? i + 1 : i], 0);
+        const double ny = __shfl_sync(FULL, ay[i + 1 < TS ? i + 1 : i], 0);
+        if (lane == 31) bx = nx, by = ny;
+      }
+      if (s < hi) {
         const uint32_t ns = s + wbase + wpre[i];
-        Route r;
-        r.ax = ax[i];
-        r.ay = ay[i];
-        r.cx = cx[i];
-        r.cy = cy[i];
-        r.bx = bx[i];
-        r.by = by[i];
-        r.cid = cid[i];
-        r.ns = ns;
-        r.flags = RT_SPLIT | (s < Slo ? RT_LOWER : 0u);
-        r.pad = 0;
-        B.route[s] = r;
-        Ox[ns + 1] = r.cx;
-        Oy[ns + 1] = r.cy;
-        Oid[ns + 1] = r.cid;
-        Wout[ns + 1] = NONE;
-        Sdo[ns] = 0ull;
-        Sdo[ns + 1] = 0ull;
+        Ox[ns] = ax[i];
+        Oy[ns] = ay[i];
+        Oid[ns] = aid[i];
+        Wout[ns] = NONE;
+        if (w[i] != NONE) {
+          if ((lane == 31 && i + 1 == TS) || s + 1 == S) {
+            const uint32_t sb = s + 1 == S ? 0u : s + 1;
+            bx = __ldcg(Tx + sb);
+            by = __ldcg(Ty + sb);
+          }
+          Route r;
+          r.ax = ax[i];
+          r.ay = ay[i];
+          r.cx = cx[i];
+          r.cy = cy[i];
+          r.bx = bx;
+          r.by = by;
+          r.cid = cid[i];
+          r.ns = ns;
+          r.flags = RT_SPLIT | (s < Slo ? RT_LOWER : 0u);
+          r.pad = 0;
+          B.route[s] = r;
+          Ox[ns + 1] = r.cx;
+          Oy[ns + 1] = r.cy;
+          Oid[ns + 1] = r.cid;
+          Wout[ns + 1] = NONE;
+          Sdo[ns] = 0ull;
+          Sdo[ns + 1] = 0ull;
+        }
       }
     }
     running += total;
