@@ -747,11 +747,18 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   // -- are issued before the step's block scan, so one memory round trip
   // overlaps the scan; the end point B of segment s is the head of s + 1,
   // taken from the neighbouring lane.
+  // The split words of the next step are loaded one step ahead.
+  uint32_t wn[TS];
+#pragma unroll
+  for (int i = 0; i < TS; ++i) wn[i] = split_of(lo + wid * 32 * TS + i * 32 + lane);
   for (uint32_t b0 = lo; b0 < hi; b0 += STEP) {
     const uint32_t g0 = b0 + wid * 32 * TS;
     uint32_t w[TS];
 #pragma unroll
-    for (int i = 0; i < TS; ++i) w[i] = split_of(g0 + i * 32 + lane);
+    for (int i = 0; i < TS; ++i) {
+      w[i] = wn[i];
+      wn[i] = split_of(g0 + STEP + i * 32 + lane);
+    }
     double ax[TS], ay[TS], cx[TS], cy[TS];
     uint32_t aid[TS], cid[TS];
 #pragma unroll
