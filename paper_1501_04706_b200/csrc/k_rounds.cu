@@ -1430,10 +1430,34 @@ __global__ void k5_emit(Bufs B, double* ox, double* oy, long long* oidx, uint64_
   const uint32_t par = c->round & 1u;
   const uint32_t h = c->S_cur;
   const uint32_t lim = h < cap ? h : (uint32_t)cap;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += gridDim.x * blockDim.x) {
-    if (ox) ox[i] = B.Tx[par][i];
-    if (oy) oy[i] = B.Ty[par][i];
-    if (oidx) oidx[i] = (long long)B.Tid[par][i];
+  const double* Tx = B.Tx[par];
+  const double* Ty = B.Ty[par];
+  const uint32_t* Tid = B.Tid[par];
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  // one CTA per SM, four independent elements per thread in flight: a hull
+  // of millions of vertices (the circle) streams at HBM rate
+  constexpr int U = 4;
+  for (; i + (U - 1) * stride < lim; i += U * stride) {
+    double vx[U], vy[U];
+    uint32_t vi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vx[u] = __ldcs(Tx + i + u * stride);
+      vy[u] = __ldcs(Ty + i + u * stride);
+      vi[u] = __ldcs(Tid + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (ox) ox[i + u * stride] = vx[u];
+      if (oy) oy[i + u * stride] = vy[u];
+      if (oidx) oidx[i + u * stride] = (long long)vi[u];
+    }
+  }
+  for (; i < lim; i += stride) {
+    if (ox) ox[i] = Tx[i];
+    if (oy) oy[i] = Ty[i];
+    if (oidx) oidx[i] = (long long)Tid[i];
   }
 }
 
@@ -1496,15 +1520,20 @@ cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s) {
   return launch_pdl(k_rounds, grid, RTPB, sizeof(RoundSmem), s, B, true);
 }
 
+#ifndef SHB_K5_GRID
+#define SHB_K5_GRID 148
+#endif
+constexpr int K5_GRID = SHB_K5_GRID, K5_TPB = 512;
+
 void launch_k5(const Bufs& B, double* ox, double* oy, long long* oidx, uint64_t cap,
                cudaStream_t s) {
 #ifdef SHB_K5_PLAIN
-  k5_emit<<<16, 256, 0, s>>>(B, ox, oy, oidx, cap);
+  k5_emit<<<K5_GRID, K5_TPB, 0, s>>>(B, ox, oy, oidx, cap);
   return;
 #endif
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(16);
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3(K5_GRID);
+  cfg.blockDim = dim3(K5_TPB);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
