@@ -464,8 +464,9 @@ def run_b200(a):
         e2e = {"value": n_total / te / 1e6, "unit": "Mpoints/s",
                "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": 16 * n_total,
+               # per rank: its hull (x, y, int64 ids) and stats; N > 1: + the merged x
                "d2h_bytes_per_step": world * (24 * len(shard.indices) + 16 * len(shard.stats))
-               + 24 * final.h,
+               + (8 * final.h if world > 1 else 0),
                "path": "hull.run_arrays -> sh_b200_hull_ex(SH_HOST_PTRS), pinned host x/y"}
 
     # --- CPU baseline (rank 0, N = 1 only): the reference on the same points ---

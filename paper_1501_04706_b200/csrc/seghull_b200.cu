@@ -343,6 +343,62 @@ void h2d_or_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, 
   }
 }
 
+// The reverse direction for a large hull (the circle: millions of vertices)
+// into pageable host memory: device chunks are copied into the pinned ring
+// and unpacked by all host cores into the caller's array while the next
+// chunks are in flight; `widen` turns the u32 vertex ids into int64.
+// Synchronous: the caller's array is complete on return.
+void d2h_ring(void* dst, const void* src, size_t n, bool widen, cudaStream_t st) {
+  const size_t esz = widen ? 4 : 8;  // source element size
+  const size_t per = H2D_CHUNK / esz;  // elements per chunk
+  const size_t nchunks = (n + per - 1) / per;
+  std::lock_guard<std::mutex> lk(g_ring.mu);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (!g_ring.buf[0]) {
+    for (int b = 0; b < H2D_NBUF; ++b) CK(cudaMallocHost((void**)&g_ring.buf[b], H2D_CHUNK));
+  }
+  if (g_ring.dev != dev) {
+    for (int b = 0; b < H2D_NBUF; ++b) {
+      if (g_ring.done[b]) cudaEventDestroy(g_ring.done[b]);
+      CK(cudaEventCreateWithFlags(&g_ring.done[b], cudaEventDisableTiming));
+    }
+    g_ring.dev = dev;
+  }
+  const char* s = (const char*)src;
+  auto issue = [&](size_t k) {
+    const int b = (int)(k % H2D_NBUF);
+    const size_t len = std::min(per, n - k * per) * esz;
+    CK(cudaMemcpyAsync(g_ring.buf[b], s + k * per * esz, len, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(g_ring.done[b], st));
+  };
+  for (size_t k = 0; k < nchunks && k < (size_t)H2D_NBUF; ++k) issue(k);
+  for (size_t k = 0; k < nchunks; ++k) {
+    const int b = (int)(k % H2D_NBUF);
+    CK(cudaEventSynchronize(g_ring.done[b]));
+    const size_t e0 = k * per, cnt = std::min(per, n - e0);
+    const long parts = 16;
+    if (widen) {
+      const uint32_t* pb = (const uint32_t*)g_ring.buf[b];
+      int64_t* d = (int64_t*)dst + e0;
+#pragma omp parallel for num_threads(8) schedule(static)
+      for (long t = 0; t < parts; ++t) {
+        const size_t a = cnt * t / parts, e = cnt * (t + 1) / parts;
+        for (size_t i = a; i < e; ++i) d[i] = (int64_t)pb[i];
+      }
+    } else {
+      const char* pb = g_ring.buf[b];
+      char* d = (char*)dst + e0 * 8;
+#pragma omp parallel for num_threads(8) schedule(static)
+      for (long t = 0; t < parts; ++t) {
+        const size_t a = cnt * 8 * t / parts, e = cnt * 8 * (t + 1) / parts;
+        std::memcpy(d + a, pb + a, e - a);
+      }
+    }
+    if (k + H2D_NBUF < nchunks) issue(k + H2D_NBUF);
+  }
+}
+
 // Runs the whole pipeline with ONE host synchronisation: H2D (host inputs),
 // K1, K2, K3, the cooperative round kernel, K5 (device outputs), and the
 // read-back of the control block + the first STATS_EAGER round stats.
@@ -545,7 +601,11 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
     if (c.status == ST_DONE) {
       // heads of the final table (CCW from P0); device outputs were written by K5
       const uint32_t par = c.round & 1u;
-      if (!out_dev && o.h) {
+      if (!out_dev && o.h * 8 >= (H2D_CHUNK >> 2)) {  // a large hull: the pinned ring
+        if (res->x) d2h_ring(res->x, ws->B.Tx[par], o.h, false, st);
+        if (res->y) d2h_ring(res->y, ws->B.Ty[par], o.h, false, st);
+        if (res->idx) d2h_ring(res->idx, ws->B.Tid[par], o.h, true, st);
+      } else if (!out_dev && o.h) {
         if (res->x) CK(cudaMemcpyAsync(res->x, ws->B.Tx[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
         if (res->y) CK(cudaMemcpyAsync(res->y, ws->B.Ty[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
         if (res->idx) {

@@ -318,7 +318,11 @@ def run_arrays(x, y, mode: int = Mode.WithPreprocess, *, ids=None, device: int |
                              flags, device, stream, ox.ctypes.data, oy.ctypes.data,
                              oi.ctypes.data, capacity, (1 << 16) if stats else 0)
     h = int(res.h)
-    r = HullResult(ox[:h].copy(), oy[:h].copy(), oi[:h].copy(), sts, ph, int(res.kept),
+    if 2 * h < capacity:  # return compact arrays, not views of the n-sized buffers
+        ox, oy, oi = ox[:h].copy(), oy[:h].copy(), oi[:h].copy()
+    else:                 # most points are on the hull (the circle): views, no second pass
+        ox, oy, oi = ox[:h], oy[:h], oi[:h]
+    r = HullResult(ox, oy, oi, sts, ph, int(res.kept),
                    int(res.rounds), int(res.kernel_launches))
     r.kernels = kt
     r.round_end_ms, r.round_phases_ms = ends
