@@ -670,7 +670,13 @@ SH_DEV void table_small(const Bufs& B, RoundSmem& sm, uint32_t S, uint32_t Slo, 
 // slots / distance maxima of their children.  Returns false on segment-table
 // overflow (every CTA returns consistently).
 #ifndef SHB_TS
-#define SHB_TS 4
+#define SHB_TS 2
+#endif
+#ifndef SHB_T1_U
+#define SHB_T1_U 8  // split-count pass: loads in flight per thread
+#endif
+#ifndef SHB_TL_PREF
+#define SHB_TL_PREF 1  // heads of the next scatter step loaded one step ahead
 #endif
 constexpr int TS = SHB_TS;
 
@@ -693,6 +699,20 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   };
   // T1: split counts of this CTA's range (total and lower chain)
   uint32_t cnt = 0, cnt_lo = 0;
+#if SHB_T1_U
+  // only the totals matter here: any mapping of [lo, hi), T1_U loads in flight
+  constexpr int U1 = SHB_T1_U;
+  for (uint32_t g0 = lo + threadIdx.x; g0 < hi; g0 += RTPB * U1) {
+    uint32_t w[U1];
+#pragma unroll
+    for (int i = 0; i < U1; ++i) w[i] = split_of(g0 + i * RTPB);
+#pragma unroll
+    for (int i = 0; i < U1; ++i) {
+      cnt += w[i] != NONE;
+      cnt_lo += w[i] != NONE && g0 + i * RTPB < Slo;
+    }
+  }
+#else
   for (uint32_t g0 = lo + wid * 32 * TS; g0 < hi; g0 += STEP) {
     uint32_t w[TS];
 #pragma unroll
@@ -704,6 +724,7 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
       cnt_lo += w[i] != NONE && s < Slo;
     }
   }
+#endif
   {
     uint32_t t1, t2;
     block_exclusive_scan(cnt, s_ws, &t1);
@@ -751,6 +772,18 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
   uint32_t wn[TS];
 #pragma unroll
   for (int i = 0; i < TS; ++i) wn[i] = split_of(lo + wid * 32 * TS + i * 32 + lane);
+#if SHB_TL_PREF
+  // the heads of the next step are loaded one step ahead too
+  double axn[TS], ayn[TS];
+  uint32_t aidn[TS];
+#pragma unroll
+  for (int i = 0; i < TS; ++i) {
+    const uint32_t s = min(lo + wid * 32 * TS + i * 32 + lane, S - 1);
+    axn[i] = __ldcg(Tx + s);
+    ayn[i] = __ldcg(Ty + s);
+    aidn[i] = __ldcg(Tid + s);
+  }
+#endif
   for (uint32_t b0 = lo; b0 < hi; b0 += STEP) {
     const uint32_t g0 = b0 + wid * 32 * TS;
     uint32_t w[TS];
@@ -761,6 +794,18 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
     }
     double ax[TS], ay[TS], cx[TS], cy[TS];
     uint32_t aid[TS], cid[TS];
+#if SHB_TL_PREF
+#pragma unroll
+    for (int i = 0; i < TS; ++i) {
+      ax[i] = axn[i];
+      ay[i] = ayn[i];
+      aid[i] = aidn[i];
+      const uint32_t s = min(g0 + STEP + i * 32 + lane, S - 1);
+      axn[i] = __ldcg(Tx + s);
+      ayn[i] = __ldcg(Ty + s);
+      aidn[i] = __ldcg(Tid + s);
+    }
+#else
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
       const uint32_t s = min(g0 + i * 32 + lane, S - 1);
@@ -768,6 +813,7 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
       ay[i] = __ldcg(Ty + s);
       aid[i] = __ldcg(Tid + s);
     }
+#endif
 #pragma unroll
     for (int i = 0; i < TS; ++i) {
       cx[i] = cy[i] = 0.0;
