@@ -541,6 +541,9 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
 constexpr int RW = RTPB / 32;          // warps per CTA
 constexpr int KR_U = LIVE_T / RCTHREADS;  // live points per consumer thread per tile
 
+#ifndef SHB_MED
+#define SHB_MED 1
+#endif
 struct RoundSmem {
   double2 lxy[LIVE_NS][LIVE_T];    // TMA ring of live points: xy          64 KB
   uint2 lis[LIVE_NS][LIVE_T];      //                          (id, seg)   32 KB
@@ -550,6 +553,12 @@ struct RoundSmem {
   unsigned long long db[NSLOT];    // CTA farthest slots: distance bits     8 KB
   SlotRec rec[NSLOT];              //                     records          32 KB
 };
+
+// medium tables reuse rt | db | rec (idle in large rounds) as one u64 array
+[[maybe_unused]] constexpr int MED_S = (int)((sizeof(Route) * SMALL_S + 8 * NSLOT + sizeof(SlotRec) * NSLOT) / 8);
+static_assert(offsetof(RoundSmem, db) == offsetof(RoundSmem, rt) + sizeof(Route) * SMALL_S &&
+              offsetof(RoundSmem, rec) == offsetof(RoundSmem, db) + 8 * NSLOT,
+              "rt, db, rec must be contiguous");
 
 // Barrier over the CTAs still working on the rounds.
 #ifndef SHB_BAR_CTR
@@ -1218,6 +1227,15 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       }
     }
     if (threadIdx.x == 0) s_off = s_coff = 0;
+#if SHB_MED
+    // medium tables (the next table fits the idle small-table smem) with
+    // several points per segment per CTA: a CTA-local running maximum per
+    // segment screens the global atomics
+    unsigned long long* mdb = reinterpret_cast<unsigned long long*>(sm.rt);
+    const bool med = !small && Sn <= (uint32_t)MED_S && (uint64_t)m >= 2ull * P * Sn;
+    if (med)
+      for (uint32_t t = threadIdx.x; t < Sn; t += RTPB) mdb[t] = 0ull;
+#endif
     __syncthreads();
     KR_MARK();  // slots cleared, run prefix built
 
@@ -1350,6 +1368,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
           for (int u = 0; u < KR_U; ++u) {
             if ((keepm >> u) & 1u) {
               const unsigned long long db = (unsigned long long)__double_as_longlong(pd[u]);
+#if SHB_MED
+              // below this CTA's running maximum: below the final one too
+              if (med && db < atomicMax(mdb + pseg[u], db)) continue;
+#endif
               if (db >= atomicMax(Sd + pseg[u], db)) candm |= 1u << u;
             }
           }
