@@ -1,0 +1,25 @@
+"""compute-sanitizer driver: a few hulls that take every round-kernel path
+(small / medium / large tables, solo tail, one-CTA inputs), checked against
+the oracle.  Run under the sanitizer on the box:
+
+    compute-sanitizer --tool memcheck python tools/sanitize.py
+    SCALE=0.2 compute-sanitizer --tool racecheck python tools/sanitize.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_1501_04706_b200 import dataio, hull  # noqa: E402
+
+k = float(os.environ.get("SCALE", "1"))  # racecheck is slow: SCALE=0.2
+cases = [("uniform", dataio.gen_uniform(int(2e6 * k), 3)), ("disk", dataio.gen_disk(int(1e6 * k), 3)),
+         ("circle", dataio.gen_circle(int(1e6 * k), 3)), ("small", dataio.gen_uniform(5_000, 3))]
+for name, (x, y) in cases:
+    for mode in (1, 2):
+        r = hull.run_arrays(x, y, mode)
+        ref = oracle.hull_run(x, y, mode)
+        ok = np.array_equal(np.asarray(r.x), np.asarray(ref.x)) and np.array_equal(np.asarray(r.y), np.asarray(ref.y))
+        print(f"{name} m{mode}: h={len(r)} rounds={r.rounds} {'ok' if ok else 'MISMATCH'}", flush=True)
