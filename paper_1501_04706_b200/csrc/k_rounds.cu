@@ -1284,7 +1284,9 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       if (use_tma && (threadIdx.x & 31) == 0) {
         for (uint32_t kk = 0; kk < ntl; ++kk) {
           const uint32_t g = kbase + kk;
-          if (kk >= (uint32_t)LIVE_NS) mbar_wait(&sm.lebar[g % LIVE_NS], ((g / LIVE_NS) - 1) & 1u);
+          // the stage's previous use (this round or an earlier one) was released;
+          // across rounds this wait returns at once (the grid barrier ordered it)
+          if (g >= (uint32_t)LIVE_NS) mbar_wait(&sm.lebar[g % LIVE_NS], ((g / LIVE_NS) - 1) & 1u);
           issue(kk);
         }
       }
