@@ -91,12 +91,12 @@ constexpr int MAX_RUNS = MAX_ROUND_BLOCKS;
 constexpr int RCWARPS = RTPB / 32 - 1;  // round kernel: consumer warps (+ 1 producer warp)
 constexpr int RCTHREADS = 32 * RCWARPS;
 #ifndef SHB_LIVE_U
-#define SHB_LIVE_U 2
+#define SHB_LIVE_U 3
 #endif
 #ifndef SHB_LIVE_NS
-#define SHB_LIVE_NS 6
+#define SHB_LIVE_NS 4
 #endif
-constexpr int LIVE_T = SHB_LIVE_U * RCTHREADS;  // live points per TMA tile of the round kernel (960)
+constexpr int LIVE_T = SHB_LIVE_U * RCTHREADS;  // live points per TMA tile of the round kernel (1440)
 constexpr int LIVE_NS = SHB_LIVE_NS;            // its ring stages
 constexpr int MAXW = 32;             // warps per CTA upper bound (shared scratch arrays)
 constexpr uint32_t SMALL_N = 16384;  // inputs up to this size take the one-CTA path (k_small_pre)
