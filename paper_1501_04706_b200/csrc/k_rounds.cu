@@ -1113,7 +1113,10 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
   }
 }
 
-constexpr uint32_t ROUND_TARGET = 1920;  // live points per active CTA before CTAs retire
+#ifndef SHB_ROUND_TARGET
+#define SHB_ROUND_TARGET 640
+#endif
+constexpr uint32_t ROUND_TARGET = SHB_ROUND_TARGET;  // live points per active CTA before CTAs retire
 #ifndef SHB_KR_REVERSE
 #define SHB_KR_REVERSE 1
 #endif
