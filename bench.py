@@ -11,14 +11,17 @@ metric "Mpoints/s and ms per 20M-point 2D hull"):
   configs[1], the paper's headline size), inputs resident in HBM.
 * N > 1 (one process per GPU, NCCL): weak scaling -- rank r owns points
   [r*20M, (r+1)*20M) of the counter-based stream gen_uniform(N*20M, 1),
-  generated on its own GPU.  Each rank hulls its shard, the shard hulls are
-  all-gathered over NVLink (NCCL), and every rank computes the final hull of
-  the gathered vertices (hull(union) == hull(union of shard hulls),
-  SURVEY.md section 8e).  `value` = all points of the job / max-over-ranks time.
+  generated on its own GPU.  Each rank's GPU hulls its shard and writes it as
+  one fixed-size payload block (SH_OUT_PAD), ONE all-gather moves the blocks
+  over NVLink (NCCL), and every rank's library merges them
+  (sh_b200_hull_gathered; hull(union) == hull(union of shard hulls), SURVEY.md
+  section 8e).  `value` = all points of the job / max-over-ranks time.
 
 Also reported (one JSON line, rank 0):
-  e2e           the same step through the public C-ABI with pinned HOST input
-                buffers (H2D of x, y and D2H of the hull inside the timed region)
+  e2e           the same step through the public API with HOST inputs (H2D of
+                x, y and D2H of the hull inside the timed region): pageable
+                numpy arrays (the reference's caller passes std::vectors), and
+                pinned buffers as a second figure
   roofline      the dominant kernel's algorithmic bytes / its CUDA-event time vs
                 the measured HBM copy peak (MEASURED_PEAKS.json)
   cpu_baseline  the reference's own CPU path (oracle/_ref: seghull::hull::run,
@@ -44,7 +47,8 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     # name: (generator, points per rank (weak) or total (strong), scaling, seed)
-    "uniform20m": ("uniform", 20_000_000, "weak", 1),
+    "uniform1m": ("uniform", 1_000_000, "weak", 1),      # BASELINE.json configs[0]
+    "uniform20m": ("uniform", 20_000_000, "weak", 1),    # configs[1]: the headline
     "disk20m": ("disk", 20_000_000, "weak", 1),
     "circle4m": ("circle", 4_000_000, "weak", 1),
     "uniform1b": ("uniform", 1_000_000_000, "strong", 1),
@@ -87,6 +91,26 @@ def shard_of(workload, world, rank):
     first = rank * n_rank
     n_rank = max(0, min(n_rank, n_total - first))
     return kind, seed, first, n_rank, n_total, scaling
+
+
+def l2_policy(a, n_rank):
+    """(flush between timed steps?, the config note saying which)."""
+    in_bytes = 16 * n_rank
+    do_flush = not a.no_l2_flush or in_bytes <= 2 * L2_BYTES
+    note = (f"flushed between timed steps ({2 * L2_BYTES >> 20} MB write); input "
+            f"16 B/pt x {n_rank}" if do_flush else
+            f"no flush: input 16 B/pt x {n_rank} = {in_bytes >> 20} MB > "
+            f"2 x {L2_BYTES >> 20} MB L2")
+    return do_flush, note
+
+
+def config_of(a, world):
+    """The workload description -- identical in both arms (b200 and reference)."""
+    kind, seed, first, n_rank, n_total, scaling = shard_of(a.workload, world, 0)
+    return {"workload": a.workload, "generator": kind, "seed": seed,
+            "points_per_gpu": n_rank, "points_total": n_total, "mode": a.mode,
+            "parallelism": f"shard{world}" + ("+allgather_merge" if world > 1 else ""),
+            "l2": l2_policy(a, n_rank)[1]}
 
 
 def peaks():
@@ -251,8 +275,7 @@ def run_reference(a):
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": scaling, "vs_baseline": value / BASELINE_MPTS,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": a.workload, "points_per_step": n, "mode": a.mode,
-                   "generator": kind, "seed": seed},
+        "config": config_of(a, world),
         "cpu_baseline": {"value": value, "unit": "Mpoints/s", "cores": cores, "kind": kindref,
                          "sample": sample},
         "e2e": {"value": value, "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
@@ -322,17 +345,6 @@ def run_b200(a):
 
     from paper_1501_04706_b200 import shard as shardmod
 
-    def merge(dh):
-        """all-gather the shard hulls (NCCL over NVLink) and hull them on every rank."""
-        def hull_with_ids(mx, my, mids):
-            m = hull.run_device(mx, my, a.mode, ids=mids, stream=sp, stats=False)
-            launches[0] += m.kernel_launches
-            return m
-        m = shardmod.merged_hull(dh, first, world, all_gather, hull_with_ids)
-        if os.environ.get("SHB_BENCH_DEBUG"):
-            print(f"[rank {rank}] shard h {dh.h} first {first} merged h {m.h}", file=sys.stderr, flush=True)
-        return m
-
     def max_over_ranks(v):
         t = torch.tensor([v], dtype=torch.float64, device="cpu" if share else dev)
         if world > 1:
@@ -346,16 +358,32 @@ def run_b200(a):
         dist.all_gather_into_tensor(o, inp.cpu())
         out.copy_(o)
 
+    def merged(px, py, out_device=True):
+        """N > 1: this rank's shard hull packed by the GPU into one payload block,
+        ONE all-gather (NCCL over NVLink), the library's merge on every rank."""
+        res, h = shardmod.merged_hull(px, py, first, n_total, world, all_gather, mode=a.mode,
+                                      out_device=out_device, stream=sp)
+        # shard: K1, K2, K3, KR, K5-pack; merge: unpack, one-CTA pre + KR, K5 (device out)
+        launches[0] += 9 if out_device else 8
+        return res, h
+
+    class _Final:
+        def __init__(self, res, h):
+            self.h = h
+            self.x, self.y, self.indices = res
+
     def step(timings=False):
+        if world > 1 and not timings:
+            res, h = merged(x, y)
+            return _Final(res, h), None
         dh = hull.run_device(x, y, a.mode, stream=sp, timings=timings, out=out)
         launches[0] += dh.kernel_launches
-        return (merge(dh) if world > 1 else dh), dh
+        return dh, dh
 
     # L2 between timed steps: by default a flush (a write of 2x L2) outside the
     # events; --no-l2-flush instead relies on inputs larger than L2 (the
     # contract's other option), refused for inputs that fit in 2x L2
-    in_bytes = 16 * n_rank
-    do_flush = not a.no_l2_flush or in_bytes <= 2 * L2_BYTES
+    do_flush, _ = l2_policy(a, n_rank)
     flush = torch.empty(2 * L2_BYTES // 4 if do_flush else 1, dtype=torch.int32, device=dev)
 
     def barrier():
@@ -366,7 +394,7 @@ def run_b200(a):
     # --- warm-up (also JIT-free: the library is prebuilt) ---
     clocks = ClockSampler(devi)
     for _ in range(a.warmup):
-        final, shard = step()
+        final, _ = step()
     # --- timed region: K steps, per-step CUDA events on the launching stream,
     #     L2 flushed between steps outside the events ---
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -378,7 +406,7 @@ def run_b200(a):
         if do_flush:
             flush.fill_(i)
         ev[i][0].record(stream)
-        final, shard = step()
+        final, _ = step()
         ev[i][1].record(stream)
     barrier()
     clocks.stop()
@@ -396,31 +424,41 @@ def run_b200(a):
         _, sh = step(timings=True)
         ks.append(sh)
     torch.cuda.synchronize()
+    shard = ks[-1]
     hbm, peak_kind = peaks()
-    st0 = ks[-1].stats
-    m1 = (st0[0].points_remaining - st0[0].segments) if st0 else 0
-    kept = ks[-1].kept
+    st0 = shard.stats
+    m1 = st0[0].points_remaining if st0 else 0
+    kept = shard.kept
     n = n_rank
     kern = {
-        # name: (algorithmic bytes per launch, mean ms)
-        "k1_extremes": (16 * n, statistics.mean(k.kernels.extremes_ms for k in ks)),
-        "k2_filter": (16 * n + n // 4, statistics.mean(k.kernels.filter_ms for k in ks)),
-        "k3_route_round1": (16 * n + n // 4 + 24 * m1,
-                            statistics.mean(k.kernels.first_round_ms for k in ks)),
+        # name: (algorithmic bytes per launch as designed, mean ms, SURVEY 8d bytes)
+        #   K1 reads x, y; K2 reads x, y and writes 2 class bits per point; K3
+        #   re-reads x, y + class bits (instead of a survivor set written by K2)
+        #   and writes the round-1 live set (24 B per survivor m1, heads excluded)
+        "k1_extremes": (16 * n, statistics.mean(k.kernels.extremes_ms for k in ks), 16 * n),
+        "k2_filter": (16 * n + n // 4, statistics.mean(k.kernels.filter_ms for k in ks),
+                      16 * n + 20 * kept),
+        "k3_route_round1": (16 * n + n // 4 + 24 * (m1 - (st0[0].segments if st0 else 0)),
+                            statistics.mean(k.kernels.first_round_ms for k in ks),
+                            24 * (kept + m1)),
     }
     dom = max(kern, key=lambda k: kern[k][1])
-    bytes_dom, ms_dom = kern[dom]
+    bytes_dom, ms_dom, survey_dom = kern[dom]
     achieved = bytes_dom / (ms_dom * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # DRAM bytes of the same kernel from one ncu --set full capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
         t = tr.get(a.workload, {}).get(dom)
-        traffic = t["dram_bytes"] if t else None
+        if t:
+            traffic = t["dram_bytes"]
+            traffic_src = "profiles/ncu_traffic.json: " + tr.get("_source", "ncu --set full")
     except Exception:
         pass
-    per_kernel = {k: {"ms": round(v[1], 5), "alg_bytes": v[0],
-                      "GB/s": round(v[0] / (v[1] * 1e-3) / 1e9, 1) if v[1] > 0 else None}
+    per_kernel = {k: {"ms": round(v[1], 5), "alg_bytes": v[0], "survey_bytes": v[2],
+                      "GB/s": round(v[0] / (v[1] * 1e-3) / 1e9, 1) if v[1] > 0 else None,
+                      "frac_survey": round(v[2] / (v[1] * 1e-3) / 1e9 / hbm, 4)
+                      if v[1] > 0 else None}
                   for k, v in kern.items()}
     per_kernel["rounds_ge2"] = {"ms": round(statistics.mean(k.kernels.rounds_ms for k in ks), 5)}
     # whole-pipeline algorithmic bytes: 32n + 20k + sum 24 (m_{r-1} + m_r)
@@ -428,46 +466,55 @@ def run_b200(a):
     b_alg = 32 * n + 20 * kept + sum(24 * (ms_list[i] + ms_list[i + 1])
                                      for i in range(len(ms_list) - 1))
 
-    # --- e2e: the public C-ABI with pinned HOST inputs (H2D + D2H inside the region) ---
+    # --- e2e: the public API with HOST inputs (H2D + D2H inside the timed region).
+    #     Primary: pageable numpy arrays, as the reference's caller passes its
+    #     std::vectors; second figure: pinned host buffers. ---
     e2e = None
     if not a.no_e2e:
-        hx = torch.empty(n_rank, dtype=torch.float64, pin_memory=True)
-        hy = torch.empty(n_rank, dtype=torch.float64, pin_memory=True)
-        hx.copy_(x)
-        hy.copy_(y)
+        hx_pg = x.cpu().numpy().copy()
+        hy_pg = y.cpu().numpy().copy()
+        hx_pin = torch.empty(n_rank, dtype=torch.float64, pin_memory=True)
+        hy_pin = torch.empty(n_rank, dtype=torch.float64, pin_memory=True)
+        hx_pin.copy_(x)
+        hy_pin.copy_(y)
         torch.cuda.synchronize()
+        d2h = [0]
 
-        def e2e_step():
-            r = hull.run_arrays(hx, hy, a.mode, device=devi, stream=sp)
-            launches_e2e[0] += r.kernel_launches
+        def e2e_step(hx, hy):
             if world > 1:
-                ids = torch.from_numpy(r.indices).to(dev)
-                rx = torch.from_numpy(r.x).to(dev)
-                ry = torch.from_numpy(r.y).to(dev)
-                dh = hull.DeviceHull(rx, ry, ids, len(r), [], None, None, 0, 0, 0)
-                m = merge(dh)
-                return m.h, m.x.cpu()
-            return len(r), r.x
-        launches_e2e = [0]
-        for _ in range(max(1, min(a.warmup, 3))):
-            e2e_step()
-        ke = max(3, min(a.steps, 10))
-        barrier()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(ke):
-            h_e, _ = e2e_step()
-        t1.record(stream)
-        barrier()
-        te = max_over_ranks(t0.elapsed_time(t1) / 1e3) / ke
-        e2e = {"value": n_total / te / 1e6, "unit": "Mpoints/s",
-               "ms_per_step": te * 1e3,
+                (mx, my, mi), h = merged(hx, hy, out_device=False)
+                d2h[0] = 24 * h
+                return h
+            r = hull.run_arrays(hx, hy, a.mode, device=devi, stream=sp)
+            launches[0] += r.kernel_launches
+            d2h[0] = 24 * len(r) + 32 * len(r.stats)  # x, y, int64 index; stats rows
+            return len(r)
+
+        def e2e_time(hx, hy):
+            for _ in range(max(1, min(a.warmup, 3))):
+                e2e_step(hx, hy)
+            ke = max(3, min(a.steps, 10))
+            barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for _ in range(ke):
+                e2e_step(hx, hy)
+            t1.record(stream)
+            barrier()
+            return max_over_ranks(t0.elapsed_time(t1) / 1e3) / ke
+
+        te = e2e_time(hx_pg, hy_pg)
+        tp = e2e_time(hx_pin, hy_pin)
+        e2e = {"value": n_total / te / 1e6, "unit": "Mpoints/s", "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": 16 * n_total,
-               # per rank: its hull (x, y, int64 ids) and stats; N > 1: + the merged x
-               "d2h_bytes_per_step": world * (24 * len(shard.indices) + 16 * len(shard.stats))
-               + (8 * final.h if world > 1 else 0),
-               "path": "hull.run_arrays -> sh_b200_hull_ex(SH_HOST_PTRS), pinned host x/y"}
+               "d2h_bytes_per_step": d2h[0] * (world if world > 1 else 1),
+               "path": ("hull.run_arrays -> sh_b200_hull_ex(SH_HOST_PTRS), pageable numpy x/y"
+                        if world == 1 else
+                        "shard.merged_hull(host shard) -> pack (SH_HOST_PTRS|SH_OUT_PAD), "
+                        "all-gather, sh_b200_hull_gathered -> host"),
+               "pinned": {"value": n_total / tp / 1e6, "ms_per_step": tp * 1e3,
+                          "path": "same call, pinned (page-locked) host x/y"}}
 
     # --- CPU baseline (rank 0, N = 1 only): the reference on the same points ---
     cpu = None
@@ -488,6 +535,14 @@ def run_b200(a):
                          f"median of {len(times)} runs after 1 warm-up",
                "ms_per_hull": tc * 1e3}
 
+    # the final hull of the last timed step, summarised for parity checks
+    fx = final.x[:final.h].cpu().numpy() if hasattr(final.x, "cpu") else np.asarray(final.x)
+    fy = final.y[:final.h].cpu().numpy() if hasattr(final.y, "cpu") else np.asarray(final.y)
+    fi = (final.indices[:final.h].cpu().numpy() if hasattr(final.indices, "cpu")
+          else np.asarray(final.indices)).astype(np.int64)
+    import hashlib
+    digest = hashlib.sha256(fx.tobytes() + fy.tobytes() + fi.tobytes()).hexdigest()
+
     if rank == 0:
         cl = clocks.summary()
         line = {
@@ -495,18 +550,17 @@ def run_b200(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": scaling,
             "vs_baseline": value / BASELINE_MPTS, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": a.workload, "generator": kind, "seed": seed,
-                       "points_per_gpu": n_rank, "points_total": n_total, "mode": a.mode,
-                       "parallelism": f"shard{world}" + ("+nccl_allgather_merge" if world > 1 else ""),
-                       "l2": (f"flushed between timed steps ({2 * L2_BYTES >> 20} MB write); input "
-                              f"16 B/pt x {n_rank}" if do_flush else
-                              f"no flush: input 16 B/pt x {n_rank} = {in_bytes >> 20} MB > "
-                              f"2 x {L2_BYTES >> 20} MB L2")},
-            "hull": {"h": final.h, "rounds": shard.rounds, "kept_after_filter": shard.kept},
+            "config": config_of(a, world),
+            "hull": {"h": final.h, "rounds": shard.rounds, "kept_after_filter": shard.kept,
+                     "sha256_x_y_idx": digest,
+                     "first": [float(fx[0]).hex(), float(fy[0]).hex()] if final.h else None},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "alg_bytes": bytes_dom, "ms": round(ms_dom, 5),
+                         "survey_bytes": survey_dom,
+                         "frac_survey": round(survey_dom / (ms_dom * 1e-3) / 1e9 / hbm, 4),
                          "per_kernel": per_kernel,
                          "pipeline": {"alg_bytes": b_alg,
                                       "floor_ms": round(b_alg / (hbm * 1e9) * 1e3, 4),

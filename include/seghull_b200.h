@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SH_B200_ABI_VERSION 2
+#define SH_B200_ABI_VERSION 3
 
 /* return codes: 0 or 1 + seghull::Errc (error.hpp:8-19) */
 enum sh_status {
@@ -61,8 +61,12 @@ enum sh_flags {
   SH_DEVICE_PTRS = 1u,    /* x, y (and idx) are device memory on `device`          */
   SH_PHASE_TIMINGS = 2u,  /* record CUDA events per phase into sh_phase_ms         */
   SH_NO_STATS = 4u,       /* skip the per-round stats read-back                    */
-  SH_OUT_DEVICE = 8u      /* out_idx/out_x/out_y are device memory on `device`:      */
+  SH_OUT_DEVICE = 8u,     /* out_idx/out_x/out_y are device memory on `device`:      */
                           /* the vertices never leave HBM (shard hulls -> gather)    */
+  SH_OUT_PAD = 16u        /* with SH_OUT_DEVICE: write ONE fixed-size payload block  */
+                          /* at out_x: {x f64[cap] | y f64[cap] | index i64[cap]},   */
+                          /* vertices then copies of vertex 0; h > cap writes NaN x  */
+                          /* and h into index[0] (see sh_b200_hull_gathered)         */
 };
 
 /* hull.hpp:35-40 SegmentStats, plus the device time at which the round ended */
@@ -122,6 +126,8 @@ typedef struct {
   uint32_t flags;
   int device;
   void* stream;         /* cudaStream_t on `device`, or NULL for a pool stream   */
+  uint64_t id_base;     /* added to every output index (a shard's first global
+                           index); 0 for a whole input                          */
 } sh_hull_request;
 
 typedef struct {
@@ -142,6 +148,62 @@ typedef struct {
 } sh_hull_result;
 
 int sh_b200_hull_ex(const sh_hull_request* req, sh_hull_result* res);
+
+/*
+ * Multi-GPU hull (SURVEY.md section 8b "sh_b200_hull_multi", 8e; hull.hpp:95
+ * with the input split over several B200s of one node).
+ * hull(union of S_g) == hull(union of hull(S_g)): every shard is hulled on
+ * its own GPU by its own host thread (own workspace, stream and pinned ring),
+ * each shard GPU writes its hull as one fixed-size payload block straight
+ * into the root GPU's gather buffer (P2P stores over NVLink/NVSwitch; a
+ * cudaMemcpyPeerAsync when the pair has no peer mapping), and the root hulls
+ * the gathered vertices with their GLOBAL input indices as ids.  Output: the
+ * same vertices and canonical (lowest) global indices as sh_b200_hull on the
+ * whole input.  Per-round stats are not returned: a sharded run has no
+ * whole-input rounds.  A shard hull larger than the first-pass block (2048
+ * vertices) is re-packed from its retained head table, not recomputed.
+ */
+typedef struct {
+  int device;        /* CUDA device that hulls this shard                      */
+  const double* x;   /* shard points: host memory, or device memory on `device` */
+  const double* y;   /*   (SH_DEVICE_PTRS)                                      */
+  uint64_t n;        /* shard size (0: skipped)                                */
+  uint64_t first;    /* global index of the shard's first point                */
+} sh_shard;
+
+typedef struct {
+  double shards_ms;  /* host wall time: all shard hulls (parallel threads)     */
+  double gather_ms;  /* ... payload blocks complete on the root                */
+  double merge_ms;   /* ... merge hull on the root, results in caller buffers  */
+  double total_ms;
+  uint32_t shards;   /* non-empty shards                                       */
+  uint64_t block_cap;/* payload block capacity used                            */
+} sh_multi_ms;
+
+/* Contiguous split of host arrays x, y over `ndev` devices (shard g =
+ * [g n/ndev, (g+1) n/ndev) on devices[g]); the merge runs on devices[0].
+ * devices may repeat (several shards on one GPU).  flags: SH_OUT_DEVICE puts
+ * the outputs in devices[0]'s memory; SH_DEVICE_PTRS is invalid here.       */
+int sh_b200_hull_multi(const double* x, const double* y, uint64_t n, int mode, uint32_t flags,
+                       const int* devices, int ndev, int64_t* out_idx, double* out_x,
+                       double* out_y, uint64_t cap, uint64_t* out_h, sh_multi_ms* times,
+                       char* err, size_t errlen);
+
+/* Explicit shard layout (e.g. shards generated on their own devices). */
+int sh_b200_hull_shards(const sh_shard* shards, int nshards, int mode, uint32_t flags,
+                        int root_device, int64_t* out_idx, double* out_x, double* out_y,
+                        uint64_t cap, uint64_t* out_h, sh_multi_ms* times, char* err,
+                        size_t errlen);
+
+/* The merge step alone, for one-process-per-GPU callers (torch.distributed):
+ * `payload` = nblocks gathered SH_OUT_PAD blocks of block_cap vertices each
+ * (device memory on `device`, e.g. the output of one all-gather); n_total =
+ * points in the whole input.  Returns SH_CAP_TOO_SMALL with *out_h = the
+ * block capacity needed when a block carries the overflow marker.           */
+int sh_b200_hull_gathered(const double* payload, uint32_t nblocks, uint64_t block_cap,
+                          uint64_t n_total, int mode, uint32_t flags, int device, void* stream,
+                          int64_t* out_idx, double* out_x, double* out_y, uint64_t cap,
+                          uint64_t* out_h, char* err, size_t errlen);
 
 /*
  * Device generators, bit-identical to the

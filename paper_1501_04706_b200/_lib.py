@@ -37,7 +37,7 @@ class sh_kernel_ms(ctypes.Structure):
 
 class sh_hull_request(ctypes.Structure):
     _fields_ = [("x", _vp), ("y", _vp), ("n", _u64), ("ids", _vp), ("mode", ctypes.c_int),
-                ("flags", _u32), ("device", ctypes.c_int), ("stream", _vp)]
+                ("flags", _u32), ("device", ctypes.c_int), ("stream", _vp), ("id_base", _u64)]
 
 
 class sh_hull_result(ctypes.Structure):
@@ -48,17 +48,30 @@ class sh_hull_result(ctypes.Structure):
                 ("err", ctypes.c_char * 256)]
 
 
+class sh_shard(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("x", _vp), ("y", _vp), ("n", _u64), ("first", _u64)]
+
+
+class sh_multi_ms(ctypes.Structure):
+    _fields_ = [("shards_ms", ctypes.c_double), ("gather_ms", ctypes.c_double),
+                ("merge_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
+                ("shards", _u32), ("block_cap", _u64)]
+
+
 # every symbol include/seghull_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sh_b200_hull", "sh_b200_hull_ex", "sh_b200_gen_uniform", "sh_b200_gen_disk",
            "sh_b200_gen_circle_host", "sh_b200_device_info", "sh_b200_release_pool",
            "sh_b200_abi_version", "sh_b200_read_pts2",
-           "sh_b200_preprocess")
+           "sh_b200_preprocess", "sh_b200_hull_multi", "sh_b200_hull_shards",
+           "sh_b200_hull_gathered")
 
 SH_HOST_PTRS = 0
 SH_DEVICE_PTRS = 1
 SH_PHASE_TIMINGS = 2
 SH_NO_STATS = 4
 SH_OUT_DEVICE = 8
+SH_OUT_PAD = 16
+ABI_VERSION = 3
 
 _lib = None
 
@@ -89,9 +102,21 @@ def load() -> ctypes.CDLL:
         L.sh_b200_preprocess.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp, _vp, _vp, _u64, _vp,
                                          _vp, ctypes.c_char_p, ctypes.c_size_t]
         L.sh_b200_preprocess.restype = ctypes.c_int
+    L.sh_b200_hull_multi.argtypes = [_vp, _vp, _u64, ctypes.c_int, _u32, _vp, ctypes.c_int, _vp,
+                                     _vp, _vp, _u64, _vp, _vp, ctypes.c_char_p, ctypes.c_size_t]
+    L.sh_b200_hull_shards.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _u32, ctypes.c_int, _vp, _vp,
+                                      _vp, _u64, _vp, _vp, ctypes.c_char_p, ctypes.c_size_t]
+    L.sh_b200_hull_gathered.argtypes = [_vp, _u32, _u64, _u64, ctypes.c_int, _u32, ctypes.c_int,
+                                        _vp, _vp, _vp, _vp, _u64, _vp, ctypes.c_char_p,
+                                        ctypes.c_size_t]
+    for f in ("sh_b200_hull_multi", "sh_b200_hull_shards", "sh_b200_hull_gathered"):
+        getattr(L, f).restype = ctypes.c_int
     L.sh_b200_release_pool.argtypes = []
     L.sh_b200_release_pool.restype = None
     L.sh_b200_abi_version.restype = ctypes.c_int
+    if L.sh_b200_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH} has ABI {L.sh_b200_abi_version()}, expected {ABI_VERSION}: "
+                          "rebuild it")
     _lib = L
     return L
 

@@ -82,11 +82,15 @@ SH_DEV bool route_point(const Route* rp, double x, double y, uint32_t id, double
 // set: one shared-memory atomicAdd per warp, no global atomics, no barrier.
 // With Oc, the survivors flagged in candm are also listed (distance,
 // position, segment) at Oc[cbase + ...] through the counter s_coff.
-template <int NP>
+// CAPPED (K3, whose runs are sized by the workspace's live capacity, not by
+// its input share): a warp whose survivors would pass `lim` writes nothing
+// and sets *ovf = ST_OVERFLOW; the host then regrows the live sets and reruns.
+template <int NP, bool CAPPED = false>
 SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py)[NP],
                        const uint32_t (&pid)[NP], const uint32_t (&pseg)[NP], uint32_t* s_off,
                        double2* Oxy, uint2* Ois, uint32_t base, const double (&pd)[NP] = {},
-                       uint32_t candm = 0, uint32_t* s_coff = nullptr, LiveCand* Oc = nullptr) {
+                       uint32_t candm = 0, uint32_t* s_coff = nullptr, LiveCand* Oc = nullptr,
+                       uint32_t lim = 0, uint32_t* ovf = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t bal[NP];
   uint32_t tot = 0;
@@ -99,6 +103,10 @@ SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py
   uint32_t off = 0;
   if (lane == 0) off = atomicAdd(s_off, tot);
   off = base + __shfl_sync(FULL, off, 0);
+  if (CAPPED && off + tot > lim) {  // warp-uniform
+    if (lane == 0) *(volatile uint32_t*)ovf = ST_OVERFLOW;
+    return;
+  }
   const uint32_t lt = lanemask_lt();
   uint32_t e[NP];
 #pragma unroll
@@ -447,7 +455,8 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
                           (db >= *(volatile unsigned long long*)&s_db[pseg[q] & 3u])) << q;
     }
     if (__any_sync(FULL, candm)) contend_tile<K3_NP>(s_db, s_rec, candm, px, py, pd, pid, pseg, lowm);
-    run_append<K3_NP>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, run_base);
+    run_append<K3_NP, true>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, run_base, pd, 0u, nullptr,
+                            nullptr, run_base + B.run_q, &c->status);
   };
   stream_input(R, n, X, Y, I, reinterpret_cast<const unsigned char*>(B.bits), false,
                [&](int s, uint32_t first, uint32_t cnt) {
@@ -460,7 +469,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
 
   // ---- flush the CTA's records to the global slots of round 2's argmax ----
   __syncthreads();
-  if (threadIdx.x == 0 && (s_off & 1u)) {  // pad the run to an even length
+  if (threadIdx.x == 0 && (s_off & 1u) && s_off < B.run_q) {  // pad the run to an even length
     Oxy[run_base + s_off] = make_double2(0.0, 0.0);
     Ois[run_base + s_off] = make_uint2(NONE, NONE);
   }
@@ -1388,7 +1397,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     __syncthreads();
     KR_MARK();  // point loop done
     if (use_tma) kbase += ntl;  // stage uses so far (phase parity of the ring)
-    if (threadIdx.x == 0 && (s_off & 1u)) {  // pad the run to an even length
+    if (threadIdx.x == 0 && (s_off & 1u) && s_off < B.run_q) {  // pad the run to an even length
       Oxy[obase + s_off] = make_double2(0.0, 0.0);
       Ois[obase + s_off] = make_uint2(NONE, NONE);
     }
@@ -1496,7 +1505,8 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
 // K5: emit the hull (segment heads in table order) into caller device memory
 // ===========================================================================
 
-__global__ void k5_emit(Bufs B, double* ox, double* oy, long long* oidx, uint64_t cap) {
+__global__ void k5_emit(Bufs B, double* ox, double* oy, long long* oidx, uint64_t cap,
+                        unsigned long long id_base) {
   const Ctl* c = B.ctl;
   pdl_wait();  // launched early (programmatic serialisation): the rounds are done
   if (c->status != ST_DONE) return;
@@ -1524,13 +1534,13 @@ __global__ void k5_emit(Bufs B, double* ox, double* oy, long long* oidx, uint64_
     for (int u = 0; u < U; ++u) {
       if (ox) ox[i + u * stride] = vx[u];
       if (oy) oy[i + u * stride] = vy[u];
-      if (oidx) oidx[i + u * stride] = (long long)vi[u];
+      if (oidx) oidx[i + u * stride] = (long long)(vi[u] + id_base);
     }
   }
   for (; i < lim; i += stride) {
     if (ox) ox[i] = Tx[i];
     if (oy) oy[i] = Ty[i];
-    if (oidx) oidx[i] = (long long)Tid[i];
+    if (oidx) oidx[i] = (long long)(Tid[i] + id_base);
   }
 }
 
@@ -1599,9 +1609,9 @@ cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s) {
 constexpr int K5_GRID = SHB_K5_GRID, K5_TPB = 512;
 
 void launch_k5(const Bufs& B, double* ox, double* oy, long long* oidx, uint64_t cap,
-               cudaStream_t s) {
+               unsigned long long id_base, cudaStream_t s) {
 #ifdef SHB_K5_PLAIN
-  k5_emit<<<K5_GRID, K5_TPB, 0, s>>>(B, ox, oy, oidx, cap);
+  k5_emit<<<K5_GRID, K5_TPB, 0, s>>>(B, ox, oy, oidx, cap, id_base);
   return;
 #endif
   cudaLaunchConfig_t cfg = {};
@@ -1613,7 +1623,7 @@ void launch_k5(const Bufs& B, double* ox, double* oy, long long* oidx, uint64_t 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k5_emit, B, ox, oy, oidx, cap);
+  cudaLaunchKernelEx(&cfg, k5_emit, B, ox, oy, oidx, cap, id_base);
 }
 
 }  // namespace shb

@@ -11,10 +11,13 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/seghull_b200.h"
@@ -32,7 +35,7 @@ cudaError_t configure_round_kernels();
 int rounds_blocks_per_sm();
 cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s);
 void launch_k5(const Bufs& B, double* ox, double* oy, long long* oidx, uint64_t cap,
-               cudaStream_t s);
+               unsigned long long id_base, cudaStream_t s);
 void launch_gen_uniform(double* x, double* y, unsigned long long first, unsigned long long count,
                         unsigned long long seed, int grid, cudaStream_t s);
 void launch_gen_disk(double* x, double* y, unsigned long long n, unsigned long long seed,
@@ -42,6 +45,10 @@ void launch_gen_disk(double* x, double* y, unsigned long long n, unsigned long l
 int gen_tile_points();
 void launch_preprocess(const Bufs& B, double* ox, double* oy, unsigned long long cap, int grid,
                        cudaStream_t s);
+void launch_k5_pack(const Bufs& B, double* blk, uint64_t cap, unsigned long long id_base,
+                    cudaStream_t s);
+void launch_unpack(const double* pay, uint32_t R, uint64_t cap, double* x, double* y,
+                   uint32_t* ids, cudaStream_t s);
 }  // namespace shb
 
 using namespace shb;
@@ -69,11 +76,26 @@ std::mutex g_mutex;
 int g_trace_round = 0;                          // debug: trace CTA 0's tiles of this round
 thread_local unsigned long long g_last_tl[33];  // debug: [0] = count, then timestamps
 thread_local std::vector<unsigned long long> g_last_ctas;  // debug: per-CTA point-phase ends
+// One entry per CUDA device, sized once (never reallocated afterwards) and
+// only read or written under g_mutex; callers get a copy.
 std::vector<DeviceInfo> g_dev;
+std::vector<size_t> g_dev_mem;  // HBM bytes per device (same lifetime and lock as g_dev)
+
+// Host->device staging ring for pageable inputs (and the reverse for large
+// hulls): pinned chunks + one event each.  Owned by a workspace, so every
+// call -- and every host thread of a multi-GPU call -- has its own ring on
+// its own device: no shared host state, no lock held across a copy.
+constexpr size_t H2D_CHUNK = 8u << 20;
+constexpr int H2D_NBUF = 4;
+struct PinnedRing {
+  char* buf[H2D_NBUF] = {};
+  cudaEvent_t done[H2D_NBUF] = {};
+};
 
 struct Workspace {
   int device = 0;
-  uint64_t n_cap = 0, s_cap = 0;
+  uint64_t n_cap = 0, s_cap = 0, live_n = 0;  // points, segments, live-set entries
+  size_t bytes = 0;                            // device bytes (arena + staging)
   bool has_stage = false, has_stage_ids = false;
   cudaStream_t stream = nullptr;
   void* arena = nullptr;
@@ -86,11 +108,18 @@ struct Workspace {
   cudaEvent_t ev[8] = {};
   size_t tiles_cap = 0;
   int stream_grid = 0, rounds_grid = 0;
+  PinnedRing ring;
 
   ~Workspace() {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);  // nothing of ours may still be in flight
+    for (int b = 0; b < H2D_NBUF; ++b) {
+      if (ring.done[b]) cudaEventSynchronize(ring.done[b]);
+      if (ring.done[b]) cudaEventDestroy(ring.done[b]);
+      if (ring.buf[b]) cudaFreeHost(ring.buf[b]);
+    }
     if (arena) cudaFree(arena);
     if (stage) cudaFree(stage);
     if (h_res) cudaFreeHost(h_res);
@@ -106,8 +135,20 @@ std::vector<std::vector<std::unique_ptr<Workspace>>> g_pool;  // free workspaces
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-DeviceInfo& device_info(int device) {
-  if ((int)g_dev.size() <= device) g_dev.resize(device + 1);
+// Caller holds g_mutex.  The device's kernels are configured on first use.
+DeviceInfo device_info_locked(int device) {
+  if (g_dev.empty()) {
+    int nd = 0;
+    CK(cudaGetDeviceCount(&nd));
+    g_dev.resize(std::max(nd, 1));
+    g_dev_mem.assign(g_dev.size(), (size_t)48 << 30);
+    for (int d = 0; d < nd; ++d) {
+      cudaDeviceProp p;
+      if (cudaGetDeviceProperties(&p, d) == cudaSuccess) g_dev_mem[d] = p.totalGlobalMem;
+    }
+    cudaGetLastError();
+  }
+  if (device < 0 || device >= (int)g_dev.size()) throw CudaFail{cudaErrorInvalidDevice, "device"};
   DeviceInfo& d = g_dev[device];
   if (!d.configured) {
     CK(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -120,17 +161,47 @@ DeviceInfo& device_info(int device) {
   return d;
 }
 
-uint64_t seg_capacity(uint64_t n) {
-  if (n + 2 <= (1ull << 27)) return n + 2;
-  return std::max<uint64_t>(1ull << 27, n / 8);
+DeviceInfo device_info(int device) {
+  std::lock_guard<std::mutex> lk(g_mutex);
+  return device_info_locked(device);
 }
 
-std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s_cap) {
+// Segment-table and live-set capacities of a fresh workspace.  Up to 2^24
+// points every point may become a head and every point may survive round 1.
+// Beyond, the tables start at n/16 segments (140 B each) and the live sets at
+// 3n/8 points (64 B each: two 24-B ping-pong sets + the 16-B contender list):
+// uniform 1B needs 55 heads and 0.23 n round-1 survivors.  An input that
+// outgrows either ends the call with ST_OVERFLOW; the call then regrows the
+// workspace to n + 2 segments and n live points and reruns (the grown
+// workspace stays in the pool for the next call).
+// SHB_SEG_CAP / SHB_LIVE_CAP (tests) cap them to force that path on small inputs.
+constexpr uint64_t LEAN_N = 1ull << 24;  // above this, tables and live sets start lean
+
+uint64_t seg_capacity(uint64_t n) {
+  uint64_t cap = n <= LEAN_N ? n + 2 : std::max<uint64_t>(LEAN_N, n / 16);
+  if (const char* e = std::getenv("SHB_SEG_CAP")) {
+    const uint64_t v = std::strtoull(e, nullptr, 10);
+    if (v >= 4096) cap = std::min(cap, v);  // >= 2 NSLOT: small tables never check
+  }
+  return cap;
+}
+
+uint64_t live_capacity(uint64_t n) {
+  uint64_t cap = n <= LEAN_N ? n : std::max<uint64_t>(LEAN_N, (3 * n / 8 + 63) & ~63ull);
+  if (const char* e = std::getenv("SHB_LIVE_CAP")) {  // tests: force K3's overflow check
+    const uint64_t v = std::strtoull(e, nullptr, 10);
+    if (v >= 4096) cap = std::min(cap, v);
+  }
+  return cap;
+}
+
+std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s_cap,
+                                          uint64_t live_cap) {
   auto ws = std::make_unique<Workspace>();
   ws->device = device;
   ws->n_cap = n_cap;
   ws->s_cap = s_cap;
-  DeviceInfo& di = device_info(device);
+  const DeviceInfo di = device_info(device);
   CK(cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking));
   for (auto& e : ws->ev) CK(cudaEventCreate(&e));
   CK(cudaMallocHost((void**)&ws->h_res, HOST_RES_BYTES));
@@ -162,7 +233,9 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   size_t o_lxy[2], o_lis[2], o_rc[2], o_tx[2], o_ty[2], o_tid[2], o_sd[3], o_sw[3];
   // live set runs: K3's CTA j owns [j*run_q, (j+1)*run_q); the rounding of
   // run_q to whole tiles costs at most one tile per CTA
-  const uint64_t LN = N + 2ull * (uint64_t)di.sm_count * Cfg3::T;
+  const uint64_t LN = std::max<uint64_t>(std::min(live_cap, N), 64) +
+                     2ull * (uint64_t)di.sm_count * Cfg3::T;
+  ws->live_n = LN;
   for (int p = 0; p < 2; ++p) {
     o_lxy[p] = take(16 * LN);
     o_lis[p] = take(8 * LN);
@@ -185,6 +258,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   const size_t o_rc1 = take(sizeof(SlotRec) * NSLOT * rows);
   const size_t o_route = take(sizeof(Route) * S);
   CK(cudaMalloc(&ws->arena, off));
+  ws->bytes = off;
   char* a = (char*)ws->arena;
   CK(cudaMemset(a, 0, o_bits));
   Bufs& B = ws->B;
@@ -226,13 +300,33 @@ void ensure_stage(Workspace& ws, bool ids) {
   ws.stage = nullptr;
   const size_t bytes = 2 * align_up(8 * ws.n_cap, 256) + (ids ? align_up(4 * ws.n_cap, 256) : 0);
   CK(cudaMalloc(&ws.stage, bytes));
+  ws.bytes += bytes;
   ws.has_stage = true;
   ws.has_stage_ids = ids;
+}
+
+// make_workspace; on failure (out of memory) drop every pooled workspace on
+// the device and retry once.
+std::unique_ptr<Workspace> make_workspace_retry(int device, uint64_t n_cap, uint64_t s_cap,
+                                                uint64_t live_cap) {
+  try {
+    return make_workspace(device, n_cap, s_cap, live_cap);
+  } catch (const CudaFail&) {
+    cudaGetLastError();
+    std::vector<std::unique_ptr<Workspace>> drop;
+    {
+      std::lock_guard<std::mutex> lk(g_mutex);
+      if ((int)g_pool.size() > device) drop.swap(g_pool[device]);
+    }
+    drop.clear();  // destructors run outside the lock
+    return make_workspace(device, n_cap, s_cap, live_cap);
+  }
 }
 
 std::unique_ptr<Workspace> acquire(int device, uint64_t n) {
   {
     std::lock_guard<std::mutex> lk(g_mutex);
+    device_info_locked(device);
     if ((int)g_pool.size() <= device) g_pool.resize(device + 1);
     auto& v = g_pool[device];
     int best = -1;
@@ -243,32 +337,32 @@ std::unique_ptr<Workspace> acquire(int device, uint64_t n) {
       v.erase(v.begin() + best);
       return ws;
     }
-    device_info(device);
   }
   const uint64_t cap = std::max<uint64_t>(n, 1u << 12);
-  try {
-    return make_workspace(device, cap, seg_capacity(cap));
-  } catch (const CudaFail&) {
-    // out of memory: drop every pooled workspace on this device and retry once
-    cudaGetLastError();
-    {
-      std::lock_guard<std::mutex> lk(g_mutex);
-      g_pool[device].clear();
-    }
-    return make_workspace(device, cap, seg_capacity(cap));
-  }
+  return make_workspace_retry(device, cap, seg_capacity(cap), live_capacity(cap));
 }
 
 void release(std::unique_ptr<Workspace> ws) {
-  std::lock_guard<std::mutex> lk(g_mutex);
-  if ((int)g_pool.size() <= ws->device) g_pool.resize(ws->device + 1);
-  auto& v = g_pool[ws->device];
-  v.push_back(std::move(ws));
-  if (v.size() > 3) {  // keep the pool bounded: drop the smallest workspace
-    size_t small = 0;
-    for (size_t i = 1; i < v.size(); ++i)
-      if (v[i]->n_cap < v[small]->n_cap) small = i;
-    v.erase(v.begin() + small);
+  std::vector<std::unique_ptr<Workspace>> drop_list;  // destroyed after the lock
+  {
+    std::lock_guard<std::mutex> lk(g_mutex);
+    if ((int)g_pool.size() <= ws->device) g_pool.resize(ws->device + 1);
+    auto& v = g_pool[ws->device];
+    v.push_back(std::move(ws));
+    // bounded by bytes (at most 3/8 of the device's HBM parked in the pool)
+    // and by count: drop the smallest workspaces first
+    size_t total = 0;
+    for (auto& w : v) total += w->bytes;
+    const size_t budget = g_dev_mem.size() > (size_t)v.back()->device
+                              ? g_dev_mem[v.back()->device] / 8 * 3 : (size_t)48 << 30;
+    while (v.size() > 1 && (v.size() > 8 || total > budget)) {
+      size_t small = 0;
+      for (size_t i = 1; i < v.size(); ++i)
+        if (v[i]->bytes < v[small]->bytes) small = i;
+      total -= v[small]->bytes;
+      drop_list.push_back(std::move(v[small]));
+      v.erase(v.begin() + small);
+    }
   }
 }
 
@@ -284,23 +378,21 @@ struct RunOut {
   std::string msg;
 };
 
+void ensure_ring(Workspace& ws) {
+  if (ws.ring.buf[0]) return;
+  for (int b = 0; b < H2D_NBUF; ++b) {
+    CK(cudaMallocHost((void**)&ws.ring.buf[b], H2D_CHUNK));
+    CK(cudaEventCreateWithFlags(&ws.ring.done[b], cudaEventDisableTiming));
+  }
+}
+
 // Host -> device copy of a caller's buffer.  Pinned (or registered) memory
 // goes straight to the copy engine.  Pageable memory would be staged by the
-// driver through one bounce buffer at ~11 GB/s; instead it is packed into
-// pinned chunks by all host cores (OpenMP) and the chunks are copied while
-// the next ones are packed (~4 chunk buffers in flight).
-constexpr size_t H2D_CHUNK = 8u << 20;
-constexpr int H2D_NBUF = 4;
-struct PinnedRing {
-  std::mutex mu;
-  char* buf[H2D_NBUF] = {};
-  cudaEvent_t done[H2D_NBUF] = {};
-  int dev = -1;
-};
-PinnedRing g_ring;
-
-void h2d_or_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, bool host,
-                 cudaStream_t st) {
+// driver through one bounce buffer at ~11 GB/s; instead it is packed into the
+// workspace's pinned chunks by the host cores (OpenMP) and each chunk is
+// copied while the next ones are packed (H2D_NBUF chunks in flight).
+void h2d_or_copy(Workspace& ws, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                 bool host, cudaStream_t st) {
   if (!host || bytes < (H2D_CHUNK >> 2)) {
     CK(cudaMemcpyAsync(dst, src, bytes, kind, st));
     return;
@@ -311,27 +403,15 @@ void h2d_or_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, 
     return;
   }
   cudaGetLastError();  // pageable pointers may leave an error on older drivers
-  std::lock_guard<std::mutex> lk(g_ring.mu);
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  if (!g_ring.buf[0]) {
-    for (int b = 0; b < H2D_NBUF; ++b) CK(cudaMallocHost((void**)&g_ring.buf[b], H2D_CHUNK));
-  }
-  if (g_ring.dev != dev) {  // events belong to a device
-    for (int b = 0; b < H2D_NBUF; ++b) {
-      if (g_ring.done[b]) cudaEventDestroy(g_ring.done[b]);
-      CK(cudaEventCreateWithFlags(&g_ring.done[b], cudaEventDisableTiming));
-      CK(cudaEventRecord(g_ring.done[b], st));
-    }
-    g_ring.dev = dev;
-  }
+  ensure_ring(ws);
+  PinnedRing& R = ws.ring;
   const char* s = (const char*)src;
   char* d = (char*)dst;
   for (size_t off = 0, k = 0; off < bytes; off += H2D_CHUNK, ++k) {
     const int b = (int)(k % H2D_NBUF);
     const size_t len = std::min(H2D_CHUNK, bytes - off);
-    CK(cudaEventSynchronize(g_ring.done[b]));  // the copy out of buf[b] finished
-    char* pb = g_ring.buf[b];
+    CK(cudaEventSynchronize(R.done[b]));  // every earlier copy out of / into buf[b] finished
+    char* pb = R.buf[b];
     const long parts = 16;
 #pragma omp parallel for num_threads(8) schedule(static)
     for (long t = 0; t < parts; ++t) {
@@ -339,55 +419,46 @@ void h2d_or_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, 
       std::memcpy(pb + a, s + off + a, e - a);
     }
     CK(cudaMemcpyAsync(d + off, pb, len, cudaMemcpyHostToDevice, st));
-    CK(cudaEventRecord(g_ring.done[b], st));
+    CK(cudaEventRecord(R.done[b], st));
   }
 }
 
 // The reverse direction for a large hull (the circle: millions of vertices)
 // into pageable host memory: device chunks are copied into the pinned ring
-// and unpacked by all host cores into the caller's array while the next
-// chunks are in flight; `widen` turns the u32 vertex ids into int64.
-// Synchronous: the caller's array is complete on return.
-void d2h_ring(void* dst, const void* src, size_t n, bool widen, cudaStream_t st) {
+// and unpacked by the host cores into the caller's array while the next
+// chunks are in flight; `widen` turns the u32 vertex ids into int64 (plus
+// id_base).  Synchronous: the caller's array is complete on return.
+void d2h_ring(Workspace& ws, void* dst, const void* src, size_t n, bool widen, uint64_t id_base,
+              cudaStream_t st) {
   const size_t esz = widen ? 4 : 8;  // source element size
   const size_t per = H2D_CHUNK / esz;  // elements per chunk
   const size_t nchunks = (n + per - 1) / per;
-  std::lock_guard<std::mutex> lk(g_ring.mu);
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  if (!g_ring.buf[0]) {
-    for (int b = 0; b < H2D_NBUF; ++b) CK(cudaMallocHost((void**)&g_ring.buf[b], H2D_CHUNK));
-  }
-  if (g_ring.dev != dev) {
-    for (int b = 0; b < H2D_NBUF; ++b) {
-      if (g_ring.done[b]) cudaEventDestroy(g_ring.done[b]);
-      CK(cudaEventCreateWithFlags(&g_ring.done[b], cudaEventDisableTiming));
-    }
-    g_ring.dev = dev;
-  }
+  ensure_ring(ws);
+  PinnedRing& R = ws.ring;
   const char* s = (const char*)src;
   auto issue = [&](size_t k) {
     const int b = (int)(k % H2D_NBUF);
     const size_t len = std::min(per, n - k * per) * esz;
-    CK(cudaMemcpyAsync(g_ring.buf[b], s + k * per * esz, len, cudaMemcpyDeviceToHost, st));
-    CK(cudaEventRecord(g_ring.done[b], st));
+    CK(cudaEventSynchronize(R.done[b]));  // an earlier H2D out of buf[b] may still run
+    CK(cudaMemcpyAsync(R.buf[b], s + k * per * esz, len, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(R.done[b], st));
   };
   for (size_t k = 0; k < nchunks && k < (size_t)H2D_NBUF; ++k) issue(k);
   for (size_t k = 0; k < nchunks; ++k) {
     const int b = (int)(k % H2D_NBUF);
-    CK(cudaEventSynchronize(g_ring.done[b]));
+    CK(cudaEventSynchronize(R.done[b]));
     const size_t e0 = k * per, cnt = std::min(per, n - e0);
     const long parts = 16;
     if (widen) {
-      const uint32_t* pb = (const uint32_t*)g_ring.buf[b];
+      const uint32_t* pb = (const uint32_t*)R.buf[b];
       int64_t* d = (int64_t*)dst + e0;
 #pragma omp parallel for num_threads(8) schedule(static)
       for (long t = 0; t < parts; ++t) {
         const size_t a = cnt * t / parts, e = cnt * (t + 1) / parts;
-        for (size_t i = a; i < e; ++i) d[i] = (int64_t)pb[i];
+        for (size_t i = a; i < e; ++i) d[i] = (int64_t)(pb[i] + id_base);
       }
     } else {
-      const char* pb = g_ring.buf[b];
+      const char* pb = R.buf[b];
       char* d = (char*)dst + e0 * 8;
 #pragma omp parallel for num_threads(8) schedule(static)
       for (long t = 0; t < parts; ++t) {
@@ -420,9 +491,9 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
     double* sy = (double*)((char*)ws.stage + align_up(8 * ws.n_cap, 256));
     uint32_t* sid = (uint32_t*)((char*)ws.stage + 2 * align_up(8 * ws.n_cap, 256));
     const cudaMemcpyKind k = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-    h2d_or_copy(sx, rq.x, 8 * n, k, host, st);
-    h2d_or_copy(sy, rq.y, 8 * n, k, host, st);
-    if (rq.ids) h2d_or_copy(sid, rq.ids, 4 * n, k, host, st);
+    h2d_or_copy(ws, sx, rq.x, 8 * n, k, host, st);
+    h2d_or_copy(ws, sy, rq.y, 8 * n, k, host, st);
+    if (rq.ids) h2d_or_copy(ws, sid, rq.ids, 4 * n, k, host, st);
     B.in_x = sx;
     B.in_y = sy;
     B.in_id = rq.ids ? sid : nullptr;
@@ -462,7 +533,10 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   B.k2_grid = (uint32_t)g2;
   // K3's CTA j owns run j of the live set: its tiles j, j + gs, ...
   const uint64_t ntiles3 = (n + Cfg3::T - 1) / Cfg3::T;
-  B.run_q = (uint32_t)((ntiles3 + gs - 1) / gs * Cfg3::T);
+  // a run holds the CTA's whole input share, or (lean live sets) an even
+  // 1/gs of the live capacity -- K3 then checks every append against it
+  B.run_q = (uint32_t)std::min<uint64_t>((ntiles3 + gs - 1) / gs * Cfg3::T,
+                                         (ws.live_n / gs) & ~1ull);
   // K1 -> K2 -> K3 -> rounds with programmatic dependent launch: no events
   // between them (per-kernel times come from device %globaltimer marks)
   launch_k1(B, ids, g1, st);
@@ -475,8 +549,12 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   }
   if (timings) CK(cudaEventRecord(ws.ev[5], st));
   const bool out_dev = (rq.flags & SH_OUT_DEVICE) != 0;
-  if (out_dev && (res.x || res.y || res.idx)) {
-    launch_k5(B, res.x, res.y, (long long*)res.idx, res.cap, st);
+  if (out_dev && (rq.flags & SH_OUT_PAD)) {
+    launch_k5_pack(B, res.x, res.cap, rq.id_base, st);
+    CK(cudaGetLastError());
+    out.launches += 1;
+  } else if (out_dev && (res.x || res.y || res.idx)) {
+    launch_k5(B, res.x, res.y, (long long*)res.idx, res.cap, rq.id_base, st);
     CK(cudaGetLastError());
     out.launches += 1;
   }
@@ -533,7 +611,11 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   return out;
 }
 
-int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
+// One hull on one device.  `keep`: on success the workspace is handed back to
+// the caller instead of the pool (the multi-GPU path re-packs from its final
+// head table when a shard hull outgrew the payload).
+int hull_impl(const sh_hull_request* rq, sh_hull_result* res,
+              std::unique_ptr<Workspace>* keep = nullptr) {
   if (!rq || !res) return SH_INVALID_ARGUMENT;
   res->h = 0;
   res->rounds = 0;
@@ -554,6 +636,9 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
   if (!rq->x || !rq->y) return SH_INVALID_ARGUMENT;
   if (rq->mode != SH_MODE_WITH_PREPROCESS && rq->mode != SH_MODE_WITHOUT_PREPROCESS)
     return SH_INVALID_ARGUMENT;
+  const bool out_dev = (rq->flags & SH_OUT_DEVICE) != 0;
+  const bool pad = (rq->flags & SH_OUT_PAD) != 0;
+  if (pad && (!out_dev || !res->x || res->cap == 0)) return SH_INVALID_ARGUMENT;
   std::unique_ptr<Workspace> ws;
   int prev_dev = 0;
   cudaGetDevice(&prev_dev);
@@ -563,10 +648,12 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
     const bool timings = (rq->flags & SH_PHASE_TIMINGS) != 0;
     cudaStream_t st = rq->stream ? (cudaStream_t)rq->stream : ws->stream;
     RunOut o = run_pipeline(*ws, *rq, *res, st, timings);
-    if (o.code == -1) {  // segment tables too small: regrow to n + 2 and rerun
+    if (o.code == -1) {  // segment tables or live sets too small: regrow to the worst case, rerun
       const int dev = ws->device;
-      ws.reset();
-      ws = make_workspace(dev, std::max<uint64_t>(n, 1u << 12), n + 2);
+      const uint64_t cap = std::max<uint64_t>(n, 1u << 12);
+      ws.reset();  // synchronises its stream before freeing anything
+      ws = make_workspace_retry(dev, cap, cap + 2, cap);
+      st = rq->stream ? (cudaStream_t)rq->stream : ws->stream;  // the old pool stream is gone
       o = run_pipeline(*ws, *rq, *res, st, timings);
       if (o.code == -1) {
         o.code = SH_INTERNAL_ERROR;
@@ -587,24 +674,28 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
     }
     const Ctl& c = *ws->h_ctl;
     if (o.h > res->cap && (res->x || res->y || res->idx)) {
+      // (pad mode: the payload already carries the NaN marker with h)
       put_err(res->err, sizeof(res->err), "output capacity too small");
-      release(std::move(ws));
+      if (keep) *keep = std::move(ws);
+      else release(std::move(ws));
       cudaSetDevice(prev_dev);
       return SH_CAP_TOO_SMALL;
     }
-    const bool out_dev = (rq->flags & SH_OUT_DEVICE) != 0;
     const bool want_stats = res->stats && res->stats_cap && !(rq->flags & SH_NO_STATS);
     const uint64_t nst =
         want_stats ? std::min<uint64_t>({o.rounds, (uint64_t)STATS_CAP, res->stats_cap}) : 0;
+    const uint64_t base = rq->id_base;
     bool sync2 = false;
     std::vector<uint32_t> ids;
-    if (c.status == ST_DONE) {
+    if (pad) {
+      // K5-pack wrote the payload block (degenerate hulls included)
+    } else if (c.status == ST_DONE) {
       // heads of the final table (CCW from P0); device outputs were written by K5
       const uint32_t par = c.round & 1u;
       if (!out_dev && o.h * 8 >= (H2D_CHUNK >> 2)) {  // a large hull: the pinned ring
-        if (res->x) d2h_ring(res->x, ws->B.Tx[par], o.h, false, st);
-        if (res->y) d2h_ring(res->y, ws->B.Ty[par], o.h, false, st);
-        if (res->idx) d2h_ring(res->idx, ws->B.Tid[par], o.h, true, st);
+        if (res->x) d2h_ring(*ws, res->x, ws->B.Tx[par], o.h, false, 0, st);
+        if (res->y) d2h_ring(*ws, res->y, ws->B.Ty[par], o.h, false, 0, st);
+        if (res->idx) d2h_ring(*ws, res->idx, ws->B.Tid[par], o.h, true, base, st);
       } else if (!out_dev && o.h) {
         if (res->x) CK(cudaMemcpyAsync(res->x, ws->B.Tx[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
         if (res->y) CK(cudaMemcpyAsync(res->y, ws->B.Ty[par], 8 * o.h, cudaMemcpyDeviceToHost, st));
@@ -622,7 +713,7 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
       for (uint64_t i = 0; i < o.h; ++i) {
         vx[i] = c.ext_x[which[i]];
         vy[i] = c.ext_y[which[i]];
-        vi[i] = c.ext_id[which[i]];
+        vi[i] = (int64_t)(c.ext_id[which[i]] + base);
       }
       if (out_dev) {
         if (res->x) CK(cudaMemcpyAsync(res->x, vx, 8 * o.h, cudaMemcpyHostToDevice, st));
@@ -643,7 +734,8 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
       sync2 = true;
     }
     if (sync2) CK(cudaStreamSynchronize(st));
-    for (uint64_t i = 0; !out_dev && res->idx && i < ids.size(); ++i) res->idx[i] = ids[i];
+    for (uint64_t i = 0; !out_dev && res->idx && i < ids.size(); ++i)
+      res->idx[i] = (int64_t)(ids[i] + base);
     for (uint64_t i = 0; i < nst; ++i) {
       res->stats[i].iteration = i + 1;
       res->stats[i].segments = ws->h_stats[i].segments;
@@ -674,22 +766,304 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res) {
       res->phases.recurse_ms = res->kernels.rounds_ms;
       res->phases.total_ms = el(0, 6);
     }
-    release(std::move(ws));
+    if (keep) *keep = std::move(ws);
+    else release(std::move(ws));
     cudaSetDevice(prev_dev);
     return SH_OK;
   } catch (const CudaFail& f) {
     put_err(res->err, sizeof(res->err),
             std::string("CUDA error: ") + cudaGetErrorString(f.err) + " at " + f.what);
     cudaGetLastError();
-    if (ws) {
-      // a failed workspace is not returned to the pool
-      ws.reset();
-    }
+    ws.reset();  // a failed workspace is not returned to the pool
     cudaSetDevice(prev_dev);
     return SH_CUDA_ERROR;
   } catch (const std::bad_alloc&) {
     put_err(res->err, sizeof(res->err), "host allocation failed");
     cudaSetDevice(prev_dev);
+    return SH_CUDA_ERROR;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU: per-shard hulls -> one payload block per
+// shard in the root GPU's memory -> merge hull with global ids.
+
+// Device scratch buffers for gathered payloads, pooled per device.
+struct DevBuf {
+  int device = 0;
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+std::vector<DevBuf> g_bufs;  // free buffers (under g_mutex)
+
+DevBuf take_buf(int device, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_mutex);
+    for (size_t i = 0; i < g_bufs.size(); ++i)
+      if (g_bufs[i].device == device && g_bufs[i].bytes >= bytes) {
+        DevBuf b = g_bufs[i];
+        g_bufs.erase(g_bufs.begin() + i);
+        return b;
+      }
+  }
+  DevBuf b;
+  b.device = device;
+  b.bytes = std::max<size_t>(bytes, 1u << 20);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  CK(cudaSetDevice(device));
+  const cudaError_t e = cudaMalloc(&b.p, b.bytes);
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) throw CudaFail{e, "cudaMalloc(gather buffer)"};
+  return b;
+}
+
+void give_buf(DevBuf b) {
+  if (!b.p) return;
+  std::lock_guard<std::mutex> lk(g_mutex);
+  g_bufs.push_back(b);
+  if (g_bufs.size() > 16) {  // bounded: free the oldest
+    DevBuf old = g_bufs.front();
+    g_bufs.erase(g_bufs.begin());
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(old.device);
+    cudaFree(old.p);
+    cudaSetDevice(cur);
+  }
+}
+
+// P2P over NVLink/NVSwitch between `dev` and `root` (both directions); false
+// when the pair cannot map each other (the caller then stages + copies).
+bool enable_peer(int dev, int root) {
+  if (dev == root) return true;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, dev, root) != cudaSuccess || !can) {
+    cudaGetLastError();
+    return false;
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(dev);
+  cudaError_t e = cudaDeviceEnablePeerAccess(root, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
+  cudaGetLastError();
+  cudaSetDevice(cur);
+  return e == cudaSuccess;
+}
+
+// The merge: R payload blocks (device memory on `device`) -> hull with
+// global ids.  Returns SH_CAP_TOO_SMALL with res->h = the block capacity the
+// largest shard hull needs when some block carries the overflow marker.
+int gathered_impl(const double* pay, uint32_t R, uint64_t bcap, uint64_t n_total, int mode,
+                  uint32_t flags, int device, void* stream, sh_hull_result* res) {
+  res->h = 0;
+  res->err[0] = 0;
+  if (!pay || R == 0 || bcap == 0) return SH_INVALID_ARGUMENT;
+  if (n_total >= 0xFFFFFFF0ull) {
+    put_err(res->err, sizeof(res->err), "run: input too large for 32-bit point ids");
+    return SH_INPUT_TOO_LARGE;
+  }
+  const uint64_t m = (uint64_t)R * bcap;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  std::unique_ptr<Workspace> ws;
+  try {
+    CK(cudaSetDevice(device));
+    ws = acquire(device, m);
+    ensure_stage(*ws, true);
+    cudaStream_t st = stream ? (cudaStream_t)stream : ws->stream;
+    double* sx = (double*)ws->stage;
+    double* sy = (double*)((char*)ws->stage + align_up(8 * ws->n_cap, 256));
+    uint32_t* sid = (uint32_t*)((char*)ws->stage + 2 * align_up(8 * ws->n_cap, 256));
+    launch_unpack(pay, R, bcap, sx, sy, sid, st);
+    CK(cudaGetLastError());
+    sh_hull_request rq;
+    std::memset(&rq, 0, sizeof(rq));
+    rq.x = sx;
+    rq.y = sy;
+    rq.ids = sid;
+    rq.n = m;
+    rq.mode = mode;
+    rq.flags = SH_DEVICE_PTRS | (flags & (SH_OUT_DEVICE | SH_NO_STATS | SH_PHASE_TIMINGS));
+    rq.device = device;
+    rq.stream = st;
+    // the staging arrays stay ours until the merge has read them
+    std::unique_ptr<Workspace> hold = std::move(ws);
+    int rc = hull_impl(&rq, res);
+    if (rc == SH_NON_FINITE_INPUT) {  // a NaN marker: which block, what it needs
+      uint64_t need = 0;
+      for (uint32_t b = 0; b < R; ++b) {
+        double x0 = 0;
+        long long h = 0;
+        CK(cudaMemcpy(&x0, pay + (uint64_t)b * 3 * bcap, 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&h, pay + (uint64_t)b * 3 * bcap + 2 * bcap, 8, cudaMemcpyDeviceToHost));
+        if (std::isnan(x0) && h > 0) need = std::max<uint64_t>(need, (uint64_t)h);
+      }
+      if (need) {
+        res->h = need;
+        put_err(res->err, sizeof(res->err), "shard hull exceeds the payload block capacity");
+        rc = SH_CAP_TOO_SMALL;
+      }
+    }
+    release(std::move(hold));
+    cudaSetDevice(prev);
+    return rc;
+  } catch (const CudaFail& f) {
+    put_err(res->err, sizeof(res->err),
+            std::string("CUDA error: ") + cudaGetErrorString(f.err) + " at " + f.what);
+    cudaGetLastError();
+    cudaSetDevice(prev);
+    return SH_CUDA_ERROR;
+  }
+}
+
+constexpr uint64_t PAYLOAD_CAP = 2048;  // shard-hull vertices per block in the first pass
+
+int shards_impl(const sh_shard* sh, int nsh, int mode, uint32_t flags, int root, int64_t* out_idx,
+                double* out_x, double* out_y, uint64_t cap, uint64_t* out_h, sh_multi_ms* tm,
+                char* err, size_t errlen) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  if (out_h) *out_h = 0;
+  if (tm) std::memset(tm, 0, sizeof(*tm));
+  if (!sh || nsh <= 0) return SH_INVALID_ARGUMENT;
+  if (mode != SH_MODE_WITH_PREPROCESS && mode != SH_MODE_WITHOUT_PREPROCESS)
+    return SH_INVALID_ARGUMENT;
+  uint64_t n_total = 0;
+  std::vector<int> live;  // non-empty shards, in order
+  for (int g = 0; g < nsh; ++g) {
+    if (sh[g].n == 0) continue;
+    if (!sh[g].x || !sh[g].y) return SH_INVALID_ARGUMENT;
+    live.push_back(g);
+    n_total = std::max<uint64_t>(n_total, sh[g].first + sh[g].n);
+  }
+  if (live.empty()) {
+    put_err(err, errlen, "run: empty point set");
+    return SH_EMPTY_INPUT;  // hull.cpp:221
+  }
+  if (n_total >= 0xFFFFFFF0ull) {
+    put_err(err, errlen, "run: input too large for 32-bit point ids");
+    return SH_INPUT_TOO_LARGE;
+  }
+  const uint32_t R = (uint32_t)live.size();
+  int prev = 0;
+  cudaGetDevice(&prev);
+  DevBuf pay;
+  std::vector<std::unique_ptr<Workspace>> kept(R);
+  try {
+    uint64_t bcap = PAYLOAD_CAP;
+    pay = take_buf(root, 24 * bcap * R);
+    std::vector<int> code(R, SH_OK);
+    std::vector<sh_hull_result> rs(R);
+    std::vector<DevBuf> local(R);  // staging blocks of shards without P2P to the root
+    std::vector<char> p2p(R, 0);
+    for (uint32_t r = 0; r < R; ++r) p2p[r] = enable_peer(sh[live[r]].device, root);
+    auto block = [&](uint32_t r) { return (double*)pay.p + (uint64_t)r * 3 * bcap; };
+    auto run_shard = [&](uint32_t r) {
+      const sh_shard& s = sh[live[r]];
+      sh_hull_request rq;
+      std::memset(&rq, 0, sizeof(rq));
+      rq.x = s.x;
+      rq.y = s.y;
+      rq.n = s.n;
+      rq.mode = mode;
+      rq.flags = (flags & SH_DEVICE_PTRS) | SH_OUT_DEVICE | SH_OUT_PAD | SH_NO_STATS;
+      rq.device = s.device;
+      rq.id_base = s.first;
+      sh_hull_result& res = rs[r];
+      std::memset(&res, 0, sizeof(res));
+      try {
+        if (!p2p[r]) local[r] = take_buf(s.device, 24 * bcap);
+      } catch (const CudaFail&) {
+        code[r] = SH_CUDA_ERROR;
+        return;
+      }
+      res.x = p2p[r] ? block(r) : (double*)local[r].p;
+      res.cap = bcap;
+      code[r] = hull_impl(&rq, &res, &kept[r]);
+    };
+    {
+      std::vector<std::thread> th;
+      for (uint32_t r = 1; r < R; ++r) th.emplace_back(run_shard, r);
+      run_shard(0);
+      for (auto& t : th) t.join();
+    }
+    const auto t1 = clk::now();
+    // errors in shard order: the first non-finite shard holds the global first index
+    for (uint32_t r = 0; r < R; ++r) {
+      if (code[r] == SH_OK || code[r] == SH_CAP_TOO_SMALL) continue;
+      std::string m = rs[r].err;
+      if (code[r] == SH_NON_FINITE_INPUT)
+        m = "run: non-finite coordinate at index " + std::to_string(rs[r].bad_index + sh[live[r]].first);
+      put_err(err, errlen, m);
+      for (auto& w : kept)
+        if (w) release(std::move(w));
+      for (auto& b : local) give_buf(b);
+      give_buf(pay);
+      cudaSetDevice(prev);
+      return code[r];
+    }
+    uint64_t need = 0;
+    for (uint32_t r = 0; r < R; ++r)
+      if (code[r] == SH_CAP_TOO_SMALL) need = std::max<uint64_t>(need, rs[r].h);
+    if (need) {  // second pass: re-pack every shard from its retained head table
+      give_buf(pay);
+      bcap = need;
+      pay = take_buf(root, 24 * bcap * R);
+      for (uint32_t r = 0; r < R; ++r) {
+        give_buf(local[r]);
+        local[r] = DevBuf{};
+        CK(cudaSetDevice(kept[r]->device));
+        if (!p2p[r]) local[r] = take_buf(kept[r]->device, 24 * bcap);
+        launch_k5_pack(kept[r]->B, p2p[r] ? block(r) : (double*)local[r].p, bcap, sh[live[r]].first,
+                       kept[r]->stream);
+        CK(cudaGetLastError());
+      }
+    }
+    for (uint32_t r = 0; r < R; ++r) {  // shards without P2P: one peer copy each
+      if (p2p[r]) continue;
+      CK(cudaSetDevice(kept[r]->device));
+      CK(cudaMemcpyPeerAsync(block(r), root, local[r].p, kept[r]->device, 24 * bcap,
+                             kept[r]->stream));
+    }
+    for (uint32_t r = 0; r < R; ++r) {
+      CK(cudaSetDevice(kept[r]->device));
+      CK(cudaStreamSynchronize(kept[r]->stream));
+    }
+    for (auto& w : kept) release(std::move(w));
+    for (auto& b : local) give_buf(b);
+    const auto t2 = clk::now();
+    sh_hull_result res;
+    std::memset(&res, 0, sizeof(res));
+    res.x = out_x;
+    res.y = out_y;
+    res.idx = out_idx;
+    res.cap = cap;
+    const int rc = gathered_impl((const double*)pay.p, R, bcap, n_total, mode,
+                                 (flags & SH_OUT_DEVICE) | SH_NO_STATS, root, nullptr, &res);
+    give_buf(pay);
+    const auto t3 = clk::now();
+    if (out_h) *out_h = res.h;
+    put_err(err, errlen, res.err);
+    if (tm) {
+      auto ms = [](clk::time_point a, clk::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+      };
+      tm->shards_ms = ms(t0, t1);
+      tm->gather_ms = ms(t1, t2);
+      tm->merge_ms = ms(t2, t3);
+      tm->total_ms = ms(t0, t3);
+      tm->shards = R;
+      tm->block_cap = bcap;
+    }
+    cudaSetDevice(prev);
+    return rc;
+  } catch (const CudaFail& f) {
+    put_err(err, errlen, std::string("CUDA error: ") + cudaGetErrorString(f.err) + " at " + f.what);
+    cudaGetLastError();
+    for (auto& w : kept) w.reset();
+    cudaSetDevice(prev);
     return SH_CUDA_ERROR;
   }
 }
@@ -715,6 +1089,54 @@ int sh_b200_debug_last_timeline(unsigned long long* out, int cap) {
 }
 
 int sh_b200_hull_ex(const sh_hull_request* req, sh_hull_result* res) { return hull_impl(req, res); }
+
+int sh_b200_hull_shards(const sh_shard* shards, int nshards, int mode, uint32_t flags,
+                        int root_device, int64_t* out_idx, double* out_x, double* out_y,
+                        uint64_t cap, uint64_t* out_h, sh_multi_ms* times, char* err,
+                        size_t errlen) {
+  return shards_impl(shards, nshards, mode, flags, root_device, out_idx, out_x, out_y, cap, out_h,
+                     times, err, errlen);
+}
+
+int sh_b200_hull_multi(const double* x, const double* y, uint64_t n, int mode, uint32_t flags,
+                       const int* devices, int ndev, int64_t* out_idx, double* out_x,
+                       double* out_y, uint64_t cap, uint64_t* out_h, sh_multi_ms* times,
+                       char* err, size_t errlen) {
+  if (out_h) *out_h = 0;
+  if (n == 0) {
+    put_err(err, errlen, "run: empty point set");
+    return SH_EMPTY_INPUT;
+  }
+  if (!x || !y || !devices || ndev <= 0 || (flags & SH_DEVICE_PTRS)) return SH_INVALID_ARGUMENT;
+  std::vector<sh_shard> sh(ndev);
+  for (int g = 0; g < ndev; ++g) {  // contiguous shards [g n / ndev, (g + 1) n / ndev)
+    const uint64_t b = n * g / ndev, e = n * (g + 1) / ndev;
+    sh[g].device = devices[g];
+    sh[g].x = x + b;
+    sh[g].y = y + b;
+    sh[g].n = e - b;
+    sh[g].first = b;
+  }
+  return shards_impl(sh.data(), ndev, mode, flags & ~(uint32_t)SH_DEVICE_PTRS, devices[0], out_idx,
+                     out_x, out_y, cap, out_h, times, err, errlen);
+}
+
+int sh_b200_hull_gathered(const double* payload, uint32_t nblocks, uint64_t block_cap,
+                          uint64_t n_total, int mode, uint32_t flags, int device, void* stream,
+                          int64_t* out_idx, double* out_x, double* out_y, uint64_t cap,
+                          uint64_t* out_h, char* err, size_t errlen) {
+  sh_hull_result res;
+  std::memset(&res, 0, sizeof(res));
+  res.x = out_x;
+  res.y = out_y;
+  res.idx = out_idx;
+  res.cap = cap;
+  const int rc = gathered_impl(payload, nblocks, block_cap, n_total, mode, flags | SH_NO_STATS,
+                               device, stream, &res);
+  if (out_h) *out_h = res.h;
+  put_err(err, errlen, res.err);
+  return rc;
+}
 
 int sh_b200_hull(const double* x, const double* y, uint64_t n, int mode, uint32_t flags,
                  int device, int64_t* out_idx, double* out_x, double* out_y, uint64_t cap,

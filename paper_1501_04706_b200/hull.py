@@ -58,6 +58,10 @@ class CudaError(RuntimeError):
     """The CUDA runtime failed (no device, out of memory, launch failure)."""
 
 
+class CapacityError(RuntimeError):
+    """SH_CAP_TOO_SMALL: an output buffer is smaller than the hull."""
+
+
 class Mode(enum.IntEnum):
     """hull.hpp:48-51"""
     WithPreprocess = 1
@@ -153,6 +157,8 @@ def _raise(rc: int, msg: str):
         raise Error(_ERRC_OF_STATUS[rc], msg)
     if rc == 101:
         raise CudaError(msg or "CUDA error")
+    if rc == 100:
+        raise CapacityError(msg or "output capacity too small")
     raise RuntimeError(f"sh_b200_hull_ex failed with status {rc}: {msg}")
 
 
@@ -186,13 +192,23 @@ def _prepare(x, y, ids):
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.ascontiguousarray(y, dtype=np.float64)
         if ids is not None:
+            if not isinstance(ids, np.ndarray):
+                raise TypeError("ids must be a host array when x and y are")
+            if ids.dtype != np.uint32:
+                ids = np.asarray(ids)
+                if ids.size and (ids.min() < 0 or ids.max() >= 2 ** 32):
+                    raise ValueError("ids must lie in [0, 2^32)")
             ids = np.ascontiguousarray(ids, dtype=np.uint32)
     else:
         import torch
         if x.dtype != torch.float64 or y.dtype != torch.float64:
             raise TypeError("tensor inputs must be float64")
-        if ids is not None and ids.dtype not in (torch.int32, torch.uint32):
-            raise TypeError("tensor ids must be 32-bit integers")
+        if ids is not None:
+            if not (hasattr(ids, "is_cuda") and ids.is_cuda == x.is_cuda
+                    and (not x.is_cuda or ids.device == x.device)):
+                raise ValueError("ids must live on the same device as x and y")
+            if ids.dtype not in (torch.int32, torch.uint32):
+                raise TypeError("tensor ids must be 32-bit integers")
     px, dx = _ptr_of(x)
     py, dy = _ptr_of(y)
     if dx != dy:
@@ -200,6 +216,8 @@ def _prepare(x, y, ids):
     n = int(x.shape[0])
     if int(y.shape[0]) != n:
         raise ValueError("x and y differ in length")
+    if ids is not None and tuple(ids.shape) != (n,):
+        raise ValueError(f"ids must have shape ({n},), got {tuple(ids.shape)}")
     return x, y, ids, px, py, dx, n
 
 
@@ -257,7 +275,8 @@ _ROW = ctypes.sizeof(_lib.sh_round_stat)
 _ZERO_PH = PhaseTimings()
 
 
-def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, stats_cap):
+def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, stats_cap,
+          id_base=0):
     L = _lib.load()
     io = getattr(_tls, "io", None)  # per-thread request/result structs, reused
     if io is None:
@@ -271,6 +290,7 @@ def _call(px, py, n, pids, mode, flags, device, stream, ox, oy, oi, capacity, st
     req.flags = flags
     req.device = int(device)
     req.stream = _lib.stream_handle(stream)
+    req.id_base = int(id_base)
     st = _stats_buffer(stats_cap)
     res.idx = oi
     res.x = ox
@@ -414,6 +434,163 @@ def preprocess_device(x, y, *, stream: int | None = None):
         _raise(rc, err.value.decode(errors="replace"))
     k = int(kept.value)
     return ox[:k], oy[:k], int(disc.value)
+
+
+# --- multi-GPU (include/seghull_b200.h sh_b200_hull_multi / _shards / _gathered) ---
+
+@dataclass(frozen=True)
+class MultiTimings:
+    """sh_multi_ms: host wall-clock milliseconds of a multi-GPU call."""
+    shards_ms: float
+    gather_ms: float
+    merge_ms: float
+    total_ms: float
+    shards: int
+    block_cap: int
+
+
+def _multi_out(cap: int, out_device, device: int):
+    if out_device:
+        import torch
+        dev = torch.device("cuda", device)
+        return (torch.empty(cap, dtype=torch.float64, device=dev),
+                torch.empty(cap, dtype=torch.float64, device=dev),
+                torch.empty(cap, dtype=torch.int64, device=dev))
+    return np.empty(cap, np.float64), np.empty(cap, np.float64), np.empty(cap, np.int64)
+
+
+def _addr(a):
+    return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+
+def _finish_multi(rc, h, bufs, err, tm=None):
+    if rc:
+        _raise(rc, err.value.decode(errors="replace"))
+    ox, oy, oi = bufs
+    r = HullResult(ox[:h], oy[:h], oi[:h])
+    if tm is not None:
+        r.kernels = MultiTimings(tm.shards_ms, tm.gather_ms, tm.merge_ms, tm.total_ms,
+                                 int(tm.shards), int(tm.block_cap))
+    return r
+
+
+def run_multi(x, y, devices, mode: int = Mode.WithPreprocess, *, cap: int | None = None,
+              out_device: bool = False) -> HullResult:
+    """Hull of host arrays x, y split contiguously over ``devices`` (one host
+    thread + workspace per shard inside the library; the merge runs on
+    devices[0]).  Same vertices and canonical global indices as :func:`run`
+    on the whole input; ``stats`` stay empty (a sharded run has no
+    whole-input rounds); ``kernels`` holds the MultiTimings."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n = int(x.size)
+    if y.shape != x.shape:
+        raise ValueError("x and y differ in length")
+    L = _lib.load()
+    devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+    cap = max(int(cap if cap is not None else min(max(n, 2), 1 << 22)), 2)
+    while True:
+        bufs = _multi_out(cap, out_device, int(devices[0]))
+        h = ctypes.c_uint64(0)
+        tm = _lib.sh_multi_ms()
+        err = ctypes.create_string_buffer(256)
+        flags = _lib.SH_HOST_PTRS | (_lib.SH_OUT_DEVICE if out_device else 0)
+        rc = L.sh_b200_hull_multi(x.ctypes.data, y.ctypes.data, n, int(mode), flags, devs,
+                                  len(devices), _addr(bufs[2]), _addr(bufs[0]), _addr(bufs[1]),
+                                  cap, ctypes.byref(h), ctypes.byref(tm), err, 256)
+        if rc == 100 and int(h.value) > cap:  # SH_CAP_TOO_SMALL: retry with the size needed
+            cap = int(h.value)
+            continue
+        return _finish_multi(rc, int(h.value), bufs, err, tm)
+
+
+def run_shards(shards, mode: int = Mode.WithPreprocess, *, root_device: int | None = None,
+               cap: int = 1 << 16, out_device: bool = False) -> HullResult:
+    """Hull of pre-placed shards: a list of (x, y, first) with x, y CUDA float64
+    tensors on their own devices (all device-resident) -- e.g. shards that each
+    GPU generated itself.  The merge runs on ``root_device`` (default: the
+    first shard's device)."""
+    L = _lib.load()
+    arr = (_lib.sh_shard * len(shards))()
+    for g, (sx, sy, first) in enumerate(shards):
+        if not (sx.is_cuda and sy.is_cuda) or sx.dtype != sy.dtype or sx.shape != sy.shape:
+            raise ValueError("run_shards needs equal-length float64 CUDA tensors per shard")
+        arr[g].device = int(sx.device.index)
+        arr[g].x, arr[g].y = sx.data_ptr(), sy.data_ptr()
+        arr[g].n, arr[g].first = int(sx.shape[0]), int(first)
+    root = int(arr[0].device if root_device is None else root_device)
+    # tensors created by torch's stream: make them complete before other streams read them
+    import torch
+    for g in range(len(shards)):
+        torch.cuda.synchronize(int(arr[g].device))
+    while True:
+        bufs = _multi_out(cap, out_device, root)
+        h = ctypes.c_uint64(0)
+        tm = _lib.sh_multi_ms()
+        err = ctypes.create_string_buffer(256)
+        flags = _lib.SH_DEVICE_PTRS | (_lib.SH_OUT_DEVICE if out_device else 0)
+        rc = L.sh_b200_hull_shards(arr, len(shards), int(mode), flags, root, _addr(bufs[2]),
+                                   _addr(bufs[0]), _addr(bufs[1]), cap, ctypes.byref(h),
+                                   ctypes.byref(tm), err, 256)
+        if rc == 100 and int(h.value) > cap:
+            cap = int(h.value)
+            continue
+        return _finish_multi(rc, int(h.value), bufs, err, tm)
+
+
+def pack_device(x, y, block, *, first: int = 0, mode: int = Mode.WithPreprocess,
+                stream: int | None = None) -> int:
+    """Hull of x, y written as ONE fixed-size payload block in device memory
+    (SH_OUT_PAD): ``block`` is a float64 CUDA tensor of 3*cap entries
+    {x[cap] | y[cap] | global index as int64 bits[cap]}; indices are offset by
+    ``first``.  x, y: CUDA float64 tensors on the block's device, or host
+    arrays (copied inside the call).  Returns h; h > cap leaves the overflow
+    marker in the block (the merge then reports the capacity needed)."""
+    import torch
+    x, y, _, px, py, dx, n = _prepare(x, y, None)
+    if not block.is_cuda or block.dtype != torch.float64:
+        raise ValueError("pack_device needs a CUDA float64 block")
+    if dx and x.device != block.device:
+        raise ValueError("x, y and the block must live on one device")
+    cap = int(block.numel()) // 3
+    if stream is None:
+        stream = torch.cuda.current_stream(block.device).cuda_stream
+    flags = ((_lib.SH_DEVICE_PTRS if dx else _lib.SH_HOST_PTRS) | _lib.SH_OUT_DEVICE
+             | _lib.SH_OUT_PAD | _lib.SH_NO_STATS)
+    try:
+        res, *_ = _call(px, py, n, None, mode, flags, int(block.device.index), stream,
+                        block.data_ptr(), None, None, cap, 0, id_base=first)
+    except CapacityError:  # the block carries the overflow marker
+        return int(_tls.io[1].h)
+    return int(res.h)
+
+
+def hull_gathered(payload, nblocks: int, n_total: int, mode: int = Mode.WithPreprocess, *,
+                  stream: int | None = None, out_device: bool = True):
+    """The merge step of a one-process-per-GPU run: ``payload`` is the
+    all-gathered float64 CUDA tensor of ``nblocks`` pack_device blocks.
+    Returns (x, y, indices) -- device tensors when out_device -- or raises
+    Error / returns None when a block overflowed: then (None, needed_cap)."""
+    import torch
+    L = _lib.load()
+    device = int(payload.device.index)
+    bcap = int(payload.numel()) // (3 * nblocks)
+    cap = max(2, nblocks * bcap)
+    bufs = _multi_out(cap, out_device, device)
+    if stream is None:
+        stream = torch.cuda.current_stream(payload.device).cuda_stream
+    h = ctypes.c_uint64(0)
+    err = ctypes.create_string_buffer(256)
+    rc = L.sh_b200_hull_gathered(payload.data_ptr(), nblocks, bcap, n_total, int(mode),
+                                 _lib.SH_OUT_DEVICE if out_device else 0, device,
+                                 _lib.stream_handle(stream), _addr(bufs[2]), _addr(bufs[0]),
+                                 _addr(bufs[1]), cap, ctypes.byref(h), err, 256)
+    if rc == 100:
+        return None, int(h.value)
+    if rc:
+        _raise(rc, err.value.decode(errors="replace"))
+    k = int(h.value)
+    return (bufs[0][:k], bufs[1][:k], bufs[2][:k]), k
 
 
 def run(points: PointSet, mode: Mode = Mode.WithPreprocess,

@@ -33,7 +33,7 @@ def test_library_loads_and_exports_header_symbols():
     for s in syms:
         assert hasattr(L, s), f"{s} declared in include/ but not exported"
     assert set(_lib.EXPORTS) == syms
-    assert L.sh_b200_abi_version() == 2
+    assert L.sh_b200_abi_version() == _lib.ABI_VERSION == 3
 
 
 def test_library_is_sm100a_cubin():
@@ -79,7 +79,20 @@ def test_host_generators_bit_identical_to_reference_stream():
     assert np.array_equal(dy.view(np.uint64), ody.view(np.uint64))
 
 
-def test_struct_layouts_match_header():
+def test_struct_layouts_match_header(tmp_path):
     assert ctypes.sizeof(_lib.sh_round_stat) == 56
     assert ctypes.sizeof(_lib.sh_phase_ms) == 32
-    assert ctypes.sizeof(_lib.sh_hull_request) == 56
+    assert ctypes.sizeof(_lib.sh_hull_request) == 64
+    # every ctypes mirror against the C compiler's view of include/seghull_b200.h
+    names = ["sh_round_stat", "sh_phase_ms", "sh_kernel_ms", "sh_hull_request", "sh_hull_result",
+             "sh_shard", "sh_multi_ms"]
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "seghull_b200.h"\nint main(void){\n' +
+                   "".join(f'printf("%zu\\n", sizeof({n}));\n' for n in names) + "return 0;}\n")
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    sizes = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                            check=True).stdout.split()]
+    for n, c_size in zip(names, sizes):
+        assert ctypes.sizeof(getattr(_lib, n)) == c_size, n

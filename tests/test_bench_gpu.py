@@ -41,3 +41,29 @@ def test_bench_two_ranks_share_one_gpu(tmp_path):
     x, y = dataio.gen_uniform_device(40_000_000, 1)
     whole = hull.run_device(x, y, 1, stats=False)
     assert line["hull"]["h"] == whole.h
+    # coordinates AND canonical global indices of the merged hull (sha256 of
+    # x bits | y bits | int64 indices) equal the one-device hull of the stream
+    import hashlib
+    import numpy as np
+    wx, wy = whole.x.cpu().numpy(), whole.y.cpu().numpy()
+    wi = whole.indices.cpu().numpy().astype(np.int64)
+    assert line["hull"]["sha256_x_y_idx"] == hashlib.sha256(
+        wx.tobytes() + wy.tobytes() + wi.tobytes()).hexdigest()
+
+
+def test_bench_single_gpu_line(tmp_path):
+    """N = 1 default workload: the line's hull equals the reference golden."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = tmp_path / "b1.json"
+    subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3",
+                    "--no-cpu-baseline", "--workload", "uniform1m", "--json-out", str(out)],
+                   cwd=ROOT, check=True, timeout=600)
+    line = json.loads(out.read_text())
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "configs.json")))["uniform_1m_s1"]
+    assert line["hull"]["h"] == g["mode1"]["h"]
+    assert line["hull"]["first"] == g["mode1"]["first"]
+    assert line["config"]["points_total"] == 1_000_000
+    assert line["e2e"]["value"] > 0 and line["e2e"]["pinned"]["value"] > 0
+    assert line["gpu_launches"] > 0

@@ -1,12 +1,15 @@
-"""Multi-GPU sharding logic on CPU: world_size 2, gloo.
+"""Multi-GPU sharding glue on CPU: world_size 2, gloo.
 
-The product path (bench.py --gpus N) runs one process per GPU over NCCL and
-hulls the gathered shard hulls with the sm_100a library.  Here the same
-host-side merge code (paper_1501_04706_b200.shard) runs on two CPU processes
-over gloo, with the oracle standing in for the per-shard hull (there is no
-GPU in this container).  Checked: hull(union of shard hulls) == hull(all),
-bit-exact coordinates, canonical GLOBAL indices, for shards with duplicates
-across ranks and with empty-looking pads (h differs per rank).
+The product path (bench.py --gpus N; shard.merged_hull) runs one process per
+GPU: the library packs each shard hull into a fixed-size payload block
+(sh_b200_hull_ex + SH_OUT_PAD), ONE all-gather moves the blocks, and the
+library merges them (sh_b200_hull_gathered).  There is no GPU here, so the two
+library steps are replaced by stand-ins that restate the payload contract of
+include/seghull_b200.h on top of the oracle; what runs for real is the glue:
+block sizing, the gloo all-gather, and the overflow protocol (a shard hull
+larger than the block leaves a marker with its size; every rank retries with
+blocks of that size).  The library steps themselves are GPU-tested
+(tests/test_multi_gpu.py, tests/test_bench_gpu.py).
 """
 import os
 import socket
@@ -29,59 +32,71 @@ def _free_port():
     return p
 
 
-class _Hull:
-    def __init__(self, x, y, idx):
-        self.x = torch.from_numpy(np.ascontiguousarray(x))
-        self.y = torch.from_numpy(np.ascontiguousarray(y))
-        self.indices = torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int64))
-
-
-def _oracle_hull(x, y, mode):
+def _pack_standin(x, y, block, *, first, mode, stream=None):
+    """SH_OUT_PAD restated: {x[cap] | y[cap] | int64 global index[cap]}, vertices
+    then copies of vertex 0; h > cap -> NaN x and h in index[0]."""
+    cap = block.numel() // 3
     r = oracle.hull_run(x, y, mode)
-    return r.x, r.y, oracle.canonical_index(x, y, r.x, r.y)
+    idx = oracle.canonical_index(x, y, r.x, r.y) + first
+    h = r.x.size
+    bx, by = block[:cap], block[cap:2 * cap]
+    bi = block[2 * cap:].view(torch.int64)
+    if h > cap:
+        bx.fill_(float("nan"))
+        by.zero_()
+        bi.zero_()
+        bi[0] = h
+        return h
+    pad = lambda v: np.concatenate([v, np.full(cap - h, v[0], v.dtype)])
+    bx.copy_(torch.from_numpy(pad(r.x)))
+    by.copy_(torch.from_numpy(pad(r.y)))
+    bi.copy_(torch.from_numpy(pad(idx.astype(np.int64))))
+    return h
 
 
-def _oracle_hull_ids(mx, my, mids, mode):
-    """The C-ABI's ids rule restated for the test: the hull of the gathered
-    points, each vertex reported with the lowest id among equal coordinates.
-    Non-finite input raises hull.Error(NonFiniteInput), like the C-ABI."""
-    from paper_1501_04706_b200 import hull
-    x, y, ids = mx.numpy(), my.numpy(), mids.numpy().astype(np.int64) & 0xFFFFFFFF
-    if not (np.isfinite(x).all() and np.isfinite(y).all()):
-        raise hull.Error(hull.Errc.NonFiniteInput, "non-finite input")
-    hx, hy, _ = _oracle_hull(x, y, mode)
-    out = []
-    for a, b in zip(hx, hy):
-        out.append(int(ids[(x == a) & (y == b)].min()))
-    return _Hull(hx, hy, np.array(out, np.int64))
+def _merge_standin(g, nblocks, n_total, mode, stream=None, out_device=True):
+    """sh_b200_hull_gathered restated: unpack, report an overflow marker, else the
+    hull of the gathered points with the lowest id among equal coordinates."""
+    cap = g.numel() // (3 * nblocks)
+    b = g.view(nblocks, 3, cap)
+    x = b[:, 0, :].reshape(-1).numpy()
+    y = b[:, 1, :].reshape(-1).numpy()
+    ids = b[:, 2, :].reshape(-1).contiguous().view(torch.int64).numpy()
+    if np.isnan(x).any():
+        need = [int(b[k, 2, :].contiguous().view(torch.int64)[0]) for k in range(nblocks)
+                if np.isnan(float(b[k, 0, 0]))]
+        return None, max(need)
+    r = oracle.hull_run(x, y, mode)
+    out = np.array([ids[(x == a) & (y == c)].min() for a, c in zip(r.x, r.y)], np.int64)
+    return (r.x, r.y, out), r.x.size
 
 
-def _worker(rank, world, port, x, y, mode, q, hmax=shard.HMAX):
+def _worker(rank, world, port, x, y, mode, q, cap):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         try:
             first, cnt = shard.shard_range(x.size, world, rank)
-            lx, ly, li = _oracle_hull(x[first:first + cnt], y[first:first + cnt], mode)
-            m = shard.merged_hull(_Hull(lx, ly, li), first, world, dist.all_gather_into_tensor,
-                                  lambda mx, my, mids: _oracle_hull_ids(mx, my, mids, mode),
-                                  hmax=hmax)
-            q.put((rank, m.x.numpy().copy(), m.y.numpy().copy(), m.indices.numpy().copy()))
+            (mx, my, mi), h = shard.merged_hull(
+                x[first:first + cnt], y[first:first + cnt], first, x.size, world,
+                dist.all_gather_into_tensor, mode=mode, block_cap=cap,
+                pack=_pack_standin, merge=_merge_standin)
+            q.put((rank, mx.copy(), my.copy(), mi.copy()))
         finally:
             dist.destroy_process_group()
     except BaseException as e:  # surface child failures instead of a queue timeout
         q.put((rank, "error", repr(e), None))
 
 
-def _run(x, y, mode, world=2, hmax=shard.HMAX):
+def _run(x, y, mode, world=2, cap=shard.HMAX):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     os.environ["PYTHONPATH"] = os.pathsep.join(
         [root, os.path.join(root, "tests"), os.environ.get("PYTHONPATH", "")])
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, x, y, mode, q, hmax))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, x, y, mode, q, cap))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -95,25 +110,26 @@ def _run(x, y, mode, world=2, hmax=shard.HMAX):
     return sorted(res, key=lambda t: t[0])
 
 
-@pytest.mark.parametrize("mode", [1, 2])
-def test_shard_merge_equals_full_hull(mode):
-    x, y = dataio.gen_uniform(60_000, 5)
+def _check(res, x, y, mode):
     ref = oracle.hull_run(x, y, mode)
     ref_idx = oracle.canonical_index(x, y, ref.x, ref.y)
-    for rank, hx, hy, hi in _run(x, y, mode):
+    for rank, hx, hy, hi in res:
         assert np.array_equal(hx.view(np.uint64), ref.x.view(np.uint64)), rank
         assert np.array_equal(hy.view(np.uint64), ref.y.view(np.uint64)), rank
         assert np.array_equal(hi, ref_idx), rank
 
 
-def test_shard_merge_fixed_gather_overflow_falls_back():
-    """Shard hulls larger than the fixed gather (hmax) send NaN payloads; the
-    merge then redoes the gather with exact sizes -- same result."""
+@pytest.mark.parametrize("mode", [1, 2])
+def test_shard_merge_equals_full_hull(mode):
+    x, y = dataio.gen_uniform(60_000, 5)
+    _check(_run(x, y, mode), x, y, mode)
+
+
+def test_shard_merge_overflow_retries_with_needed_capacity():
+    """Shard hulls larger than the block leave the overflow marker; every rank
+    sees it in the gathered payload and retries with the size needed."""
     x, y = dataio.gen_circle(2_000, 3)  # every point is a hull vertex
-    ref = oracle.hull_run(x, y, 1)
-    for rank, hx, hy, hi in _run(x, y, 1, hmax=64):
-        assert np.array_equal(hx.view(np.uint64), ref.x.view(np.uint64)), rank
-        assert np.array_equal(hi, oracle.canonical_index(x, y, ref.x, ref.y)), rank
+    _check(_run(x, y, 1, cap=64), x, y, 1)
 
 
 def test_shard_merge_duplicates_across_ranks():
@@ -121,11 +137,9 @@ def test_shard_merge_duplicates_across_ranks():
     # ranks, the merged hull must report the rank-0 (lowest) global index
     x, y = dataio.gen_circle(3_000, 9)
     X, Y = np.concatenate([x, x]), np.concatenate([y, y])
-    ref = oracle.hull_run(X, Y, 1)
-    for rank, hx, hy, hi in _run(X, Y, 1):
-        assert np.array_equal(hx.view(np.uint64), ref.x.view(np.uint64))
-        assert np.array_equal(hi, oracle.canonical_index(X, Y, ref.x, ref.y))
-        assert hi.max() < x.size
+    res = _run(X, Y, 1)
+    _check(res, X, Y, 1)
+    assert all(r[3].max() < x.size for r in res)
 
 
 def test_shard_range_covers():
