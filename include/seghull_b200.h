@@ -253,6 +253,57 @@ int sh_b200_preprocess(const double* x, const double* y, uint64_t n, int device,
                        double* out_x, double* out_y, uint64_t cap, uint64_t* kept,
                        uint64_t* discarded, char* err, size_t errlen);
 
+/*
+ * Per-phase device APIs (hull.hpp:61-91): the
+ * reference's stages over a device HullState in the REFERENCE's layout
+ * (hull.hpp:19-33) -- rows laid out by first_split as the lower chain sorted
+ * lex-ascending then the upper chain lex-descending, head/keys/first_pts/flag
+ * as i32 -- so the reference's per-stage tests (tests/test_hull.cpp:88-314)
+ * run against the device bit for bit.  The fused path (sh_b200_hull) does not
+ * use them.  All columns are caller-owned device memory on `device` with
+ * `cap` rows; calls are ordered on `stream` (NULL: the legacy default stream)
+ * and return SH_OK, SH_INVALID_ARGUMENT, SH_CAP_TOO_SMALL or SH_CUDA_ERROR
+ * (first_split also SH_EMPTY_INPUT / SH_DEGENERATE_INPUT, hull.cpp:103-110).
+ * compute_distances / split_segments / mark_interior are asynchronous;
+ * first_split, find_farthest and compact synchronise (they return counts).
+ */
+typedef struct {
+  double* x;
+  double* y;
+  double* dist;        /* signed outward measure vs the segment's base line */
+  int32_t* head;       /* 1 at segment starts                               */
+  int32_t* keys;       /* segment id per row                                */
+  int32_t* first_pts;  /* row of the row's segment head                     */
+  int32_t* flag;       /* 1 = survives the next compaction                  */
+  uint64_t n;          /* rows in use (set by first_split and compact)      */
+  uint64_t cap;        /* rows every column can hold                        */
+} sh_hull_state;
+
+/* primitives::SegmentMax (primitives.hpp:24-30) */
+typedef struct {
+  int32_t key;
+  int32_t pad;
+  double value;
+  uint64_t index;      /* smallest row attaining value within the segment   */
+} sh_segment_max;
+
+/* hull::first_split (hull.cpp:101-158): x, y device arrays of n points */
+int sh_b200_first_split(const double* x, const double* y, uint64_t n, sh_hull_state* st,
+                        int device, void* stream, char* err, size_t errlen);
+/* hull::compute_distances (hull.cpp:160-180) */
+int sh_b200_compute_distances(const sh_hull_state* st, int device, void* stream);
+/* hull::find_farthest (hull.cpp:182-184, primitives.cpp:108-136): one entry
+ * per segment into device array out[cap]; *nseg = segments */
+int sh_b200_find_farthest(const sh_hull_state* st, sh_segment_max* out, uint64_t cap,
+                          uint64_t* nseg, int device, void* stream);
+/* hull::split_segments (hull.cpp:186-194): farthest = device array of m */
+int sh_b200_split_segments(const sh_hull_state* st, const sh_segment_max* farthest, uint64_t m,
+                           int device, void* stream);
+/* hull::mark_interior (hull.cpp:196-201) */
+int sh_b200_mark_interior(const sh_hull_state* st, int device, void* stream);
+/* hull::compact (hull.cpp:203-217): st->n shrinks; *removed = rows dropped */
+int sh_b200_compact(sh_hull_state* st, uint64_t* removed, int device, void* stream);
+
 /* Library/device information; returns SH_OK or SH_CUDA_ERROR. */
 int sh_b200_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                         uint64_t* hbm_bytes, char* name, size_t namelen);

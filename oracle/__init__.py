@@ -147,8 +147,96 @@ def ref():
                                               ctypes.c_size_t]
         L.ref_read_points_binary.argtypes = [ctypes.c_char_p, vp, vp, _u64, vp, ctypes.c_char_p,
                                              ctypes.c_size_t]
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        L.ref_state_first_split.argtypes = [vp, vp, _u64, ctypes.POINTER(ctypes.c_int)]
+        L.ref_state_first_split.restype = vp
+        L.ref_state_new.argtypes = [_u64, vp, vp, vp, vp, vp, vp, vp]
+        L.ref_state_new.restype = vp
+        L.ref_state_free.argtypes = [vp]
+        L.ref_state_size.argtypes = [vp]
+        L.ref_state_size.restype = _u64
+        L.ref_state_get.argtypes = [vp] * 8
+        for f in ("ref_state_compute_distances", "ref_state_mark_interior"):
+            getattr(L, f).argtypes = [vp]
+        L.ref_state_find_farthest.argtypes = [vp, vp, vp, vp, _u64]
+        L.ref_state_find_farthest.restype = _u64
+        L.ref_state_split_segments.argtypes = [vp, vp, vp, vp, _u64]
+        L.ref_state_compact.argtypes = [vp]
+        L.ref_state_compact.restype = _u64
+        del i32p
         _ref = L
     return _ref
+
+
+STATE_COLUMNS = ("x", "y", "dist", "head", "keys", "first_pts", "flag")
+
+
+class RefHullState:
+    """The reference's own hull::HullState driven through hull.hpp:61-91
+    (test infrastructure: pins the device per-phase API)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def first_split(cls, x, y):
+        x, y = _xy(x, y)
+        code = ctypes.c_int(0)
+        h = ref().ref_state_first_split(_ptr(x), _ptr(y), x.size, ctypes.byref(code))
+        if not h:
+            raise OracleError(code.value, "first_split")
+        return cls(h)
+
+    @classmethod
+    def from_columns(cls, **cols):
+        c = _state_cols(cols)
+        n = c["x"].size
+        return cls(ref().ref_state_new(n, *[_ptr(c[k]) for k in STATE_COLUMNS]))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            ref().ref_state_free(self._h)
+            self._h = None
+
+    def size(self) -> int:
+        return int(ref().ref_state_size(self._h))
+
+    def columns(self) -> dict:
+        n = self.size()
+        c = {k: np.empty(n, np.float64 if k in ("x", "y", "dist") else np.int32)
+             for k in STATE_COLUMNS}
+        ref().ref_state_get(self._h, *[_ptr(c[k]) for k in STATE_COLUMNS])
+        return c
+
+    def compute_distances(self):
+        ref().ref_state_compute_distances(self._h)
+
+    def find_farthest(self):
+        n = self.size()
+        k = np.empty(max(n, 1), np.int32)
+        v = np.empty(max(n, 1), np.float64)
+        i = np.empty(max(n, 1), np.uint64)
+        m = int(ref().ref_state_find_farthest(self._h, _ptr(k), _ptr(v), _ptr(i), max(n, 1)))
+        return k[:m].copy(), v[:m].copy(), i[:m].copy()
+
+    def split_segments(self, key, value, index):
+        key = np.ascontiguousarray(key, np.int32)
+        value = np.ascontiguousarray(value, np.float64)
+        index = np.ascontiguousarray(index, np.uint64)
+        ref().ref_state_split_segments(self._h, _ptr(key), _ptr(value), _ptr(index), key.size)
+
+    def mark_interior(self):
+        ref().ref_state_mark_interior(self._h)
+
+    def compact(self) -> int:
+        return int(ref().ref_state_compact(self._h))
+
+
+def _state_cols(cols):
+    out = {}
+    for k in STATE_COLUMNS:
+        out[k] = np.ascontiguousarray(cols[k], np.float64 if k in ("x", "y", "dist") else np.int32)
+    return out
 
 
 def _xy(x, y):

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <exception>
 #include <string>
+#include <vector>
 
 #include "seghull/dataio.hpp"
 #include "seghull/error.hpp"
@@ -181,6 +182,80 @@ int ref_read_points_binary(const char* path, double* x, double* y, std::uint64_t
     put_err(err, errlen, e.what());
     return 1 + static_cast<int>(e.code());
   }
+}
+
+// --- the per-phase API of hull.hpp:61-91 on a reference HullState ---------
+// (pins the device per-phase API, include/seghull_b200.h sh_b200_first_split..)
+
+void* ref_state_first_split(const double* x, const double* y, std::uint64_t n, int* code) {
+  try {
+    *code = 0;
+    return new hull::HullState(hull::first_split(make_set(x, y, n), Backend::Sequential));
+  } catch (const Error& e) {
+    *code = 1 + static_cast<int>(e.code());
+    return nullptr;
+  }
+}
+
+void* ref_state_new(std::uint64_t n, const double* x, const double* y, const double* dist,
+                    const std::int32_t* head, const std::int32_t* keys, const std::int32_t* first,
+                    const std::int32_t* flag) {
+  auto* s = new hull::HullState;
+  s->x.assign(x, x + n);
+  s->y.assign(y, y + n);
+  s->dist.assign(dist, dist + n);
+  s->head.assign(head, head + n);
+  s->keys.assign(keys, keys + n);
+  s->first_pts.assign(first, first + n);
+  s->flag.assign(flag, flag + n);
+  return s;
+}
+
+void ref_state_free(void* s) { delete static_cast<hull::HullState*>(s); }
+
+std::uint64_t ref_state_size(void* s) { return static_cast<hull::HullState*>(s)->size(); }
+
+void ref_state_get(void* sp, double* x, double* y, double* dist, std::int32_t* head,
+                   std::int32_t* keys, std::int32_t* first, std::int32_t* flag) {
+  const auto& s = *static_cast<hull::HullState*>(sp);
+  const std::size_t n = s.size();
+  std::memcpy(x, s.x.data(), 8 * n);
+  std::memcpy(y, s.y.data(), 8 * n);
+  std::memcpy(dist, s.dist.data(), 8 * n);
+  std::memcpy(head, s.head.data(), 4 * n);
+  std::memcpy(keys, s.keys.data(), 4 * n);
+  std::memcpy(first, s.first_pts.data(), 4 * n);
+  std::memcpy(flag, s.flag.data(), 4 * n);
+}
+
+void ref_state_compute_distances(void* s) {
+  hull::compute_distances(*static_cast<hull::HullState*>(s), Backend::Sequential);
+}
+
+std::uint64_t ref_state_find_farthest(void* s, std::int32_t* key, double* value,
+                                      std::uint64_t* index, std::uint64_t cap) {
+  const auto far = hull::find_farthest(*static_cast<hull::HullState*>(s), Backend::Sequential);
+  for (std::size_t j = 0; j < far.size() && j < cap; ++j) {
+    key[j] = far[j].key;
+    value[j] = far[j].value;
+    index[j] = far[j].index;
+  }
+  return far.size();
+}
+
+void ref_state_split_segments(void* s, const std::int32_t* key, const double* value,
+                              const std::uint64_t* index, std::uint64_t m) {
+  std::vector<primitives::SegmentMax> far(m);
+  for (std::size_t j = 0; j < m; ++j) far[j] = {key[j], value[j], index[j]};
+  hull::split_segments(*static_cast<hull::HullState*>(s), far, Backend::Sequential);
+}
+
+void ref_state_mark_interior(void* s) {
+  hull::mark_interior(*static_cast<hull::HullState*>(s), Backend::Sequential);
+}
+
+std::uint64_t ref_state_compact(void* s) {
+  return hull::compact(*static_cast<hull::HullState*>(s), Backend::Sequential);
 }
 
 }  // extern "C"

@@ -58,12 +58,24 @@ class sh_multi_ms(ctypes.Structure):
                 ("shards", _u32), ("block_cap", _u64)]
 
 
+class sh_hull_state(ctypes.Structure):
+    _fields_ = [("x", _vp), ("y", _vp), ("dist", _vp), ("head", _vp), ("keys", _vp),
+                ("first_pts", _vp), ("flag", _vp), ("n", _u64), ("cap", _u64)]
+
+
+class sh_segment_max(ctypes.Structure):
+    _fields_ = [("key", ctypes.c_int32), ("pad", ctypes.c_int32), ("value", ctypes.c_double),
+                ("index", _u64)]
+
+
 # every symbol include/seghull_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sh_b200_hull", "sh_b200_hull_ex", "sh_b200_gen_uniform", "sh_b200_gen_disk",
            "sh_b200_gen_circle_host", "sh_b200_device_info", "sh_b200_release_pool",
            "sh_b200_abi_version", "sh_b200_read_pts2",
            "sh_b200_preprocess", "sh_b200_hull_multi", "sh_b200_hull_shards",
-           "sh_b200_hull_gathered")
+           "sh_b200_hull_gathered", "sh_b200_first_split", "sh_b200_compute_distances",
+           "sh_b200_find_farthest", "sh_b200_split_segments", "sh_b200_mark_interior",
+           "sh_b200_compact")
 
 SH_HOST_PTRS = 0
 SH_DEVICE_PTRS = 1
@@ -109,7 +121,17 @@ def load() -> ctypes.CDLL:
     L.sh_b200_hull_gathered.argtypes = [_vp, _u32, _u64, _u64, ctypes.c_int, _u32, ctypes.c_int,
                                         _vp, _vp, _vp, _vp, _u64, _vp, ctypes.c_char_p,
                                         ctypes.c_size_t]
-    for f in ("sh_b200_hull_multi", "sh_b200_hull_shards", "sh_b200_hull_gathered"):
+    sp = ctypes.POINTER(sh_hull_state)
+    L.sh_b200_first_split.argtypes = [_vp, _vp, _u64, sp, ctypes.c_int, _vp, ctypes.c_char_p,
+                                      ctypes.c_size_t]
+    L.sh_b200_compute_distances.argtypes = [sp, ctypes.c_int, _vp]
+    L.sh_b200_find_farthest.argtypes = [sp, _vp, _u64, _vp, ctypes.c_int, _vp]
+    L.sh_b200_split_segments.argtypes = [sp, _vp, _u64, ctypes.c_int, _vp]
+    L.sh_b200_mark_interior.argtypes = [sp, ctypes.c_int, _vp]
+    L.sh_b200_compact.argtypes = [sp, _vp, ctypes.c_int, _vp]
+    for f in ("sh_b200_hull_multi", "sh_b200_hull_shards", "sh_b200_hull_gathered",
+              "sh_b200_first_split", "sh_b200_compute_distances", "sh_b200_find_farthest",
+              "sh_b200_split_segments", "sh_b200_mark_interior", "sh_b200_compact"):
         getattr(L, f).restype = ctypes.c_int
     L.sh_b200_release_pool.argtypes = []
     L.sh_b200_release_pool.restype = None

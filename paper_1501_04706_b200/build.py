@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libseghull_b200.so")
-SOURCES = ["k_pre.cu", "k_rounds.cu", "k_gen.cu", "k_gather.cu", "seghull_b200.cu", "pts2_io.cu"]
+SOURCES = ["k_pre.cu", "k_rounds.cu", "k_gen.cu", "k_gather.cu", "seghull_b200.cu", "pts2_io.cu",
+           "phases.cu"]
 HEADERS = ["device_common.cuh", "hull_kernels.cuh"]
 
 NVCC_FLAGS = [

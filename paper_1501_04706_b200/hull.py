@@ -593,6 +593,167 @@ def hull_gathered(payload, nblocks: int, n_total: int, mode: int = Mode.WithPrep
     return (bufs[0][:k], bufs[1][:k], bufs[2][:k]), k
 
 
+# --- per-phase device API (hull.hpp:61-91; include/seghull_b200.h) -----------
+
+_STATE_COLS = ("x", "y", "dist", "head", "keys", "first_pts", "flag")
+
+
+@dataclass(frozen=True)
+class SegmentMax:
+    """primitives::SegmentMax (primitives.hpp:24-30)."""
+    key: int
+    value: float
+    index: int
+
+
+class HullState:
+    """hull::HullState (hull.hpp:19-33) in HBM: one CUDA tensor per column,
+    ``cap`` rows each, the first ``n`` in use.  Driven by first_split,
+    compute_distances, find_farthest, split_segments, mark_interior and
+    compact below, each one C-ABI call into libseghull_b200.so."""
+
+    def __init__(self, cap: int, device: int = 0):
+        import torch
+        dev = torch.device("cuda", device)
+        cap = max(int(cap), 1)
+        f8 = dict(dtype=torch.float64, device=dev)
+        i4 = dict(dtype=torch.int32, device=dev)
+        self.x, self.y, self.dist = (torch.empty(cap, **f8) for _ in range(3))
+        self.head, self.keys, self.first_pts, self.flag = (torch.empty(cap, **i4) for _ in range(4))
+        self.device = device
+        self._s = _lib.sh_hull_state()
+        for k in _STATE_COLS:
+            setattr(self._s, k, getattr(self, k).data_ptr())
+        self._s.n = 0
+        self._s.cap = cap
+
+    @classmethod
+    def from_columns(cls, device: int = 0, **cols) -> "HullState":
+        """A state built from host columns (the reference tests' hand-made states)."""
+        import torch
+        n = len(cols["x"])
+        st = cls(n, device)
+        for k in _STATE_COLS:
+            dt = np.float64 if k in ("x", "y", "dist") else np.int32
+            getattr(st, k)[:n].copy_(torch.from_numpy(np.ascontiguousarray(cols[k], dt)))
+        st._s.n = n
+        return st
+
+    @property
+    def n(self) -> int:
+        return int(self._s.n)
+
+    def size(self) -> int:
+        return self.n
+
+    def segments(self) -> int:
+        return 0 if self.n == 0 else int(self.keys[self.n - 1].item()) + 1
+
+    def point(self, i: int) -> Point:
+        return Point(float(self.x[i].item()), float(self.y[i].item()))
+
+    def columns(self) -> dict:
+        """Host copies of the n rows of every column."""
+        return {k: getattr(self, k)[:self.n].cpu().numpy() for k in _STATE_COLS}
+
+    def _stream(self):
+        import torch
+        return _lib.stream_handle(torch.cuda.current_stream(self.device).cuda_stream)
+
+
+def _phase_rc(rc: int, what: str, msg: str = ""):
+    if rc:
+        _raise(rc, msg or what)
+
+
+def first_split(x, y, *, device: int | None = None) -> HullState:
+    """hull::first_split (hull.cpp:101-158): float64 CUDA tensors, or host
+    arrays (uploaded first)."""
+    import torch
+    if isinstance(x, np.ndarray) or not getattr(x, "is_cuda", False):
+        dev = 0 if device is None else device
+        x = torch.as_tensor(np.ascontiguousarray(x, np.float64)).to(f"cuda:{dev}")
+        y = torch.as_tensor(np.ascontiguousarray(y, np.float64)).to(f"cuda:{dev}")
+    x, y = x.contiguous(), y.contiguous()
+    st = HullState(int(x.shape[0]), int(x.device.index))
+    err = ctypes.create_string_buffer(256)
+    rc = _lib.load().sh_b200_first_split(x.data_ptr(), y.data_ptr(), int(x.shape[0]),
+                                         ctypes.byref(st._s), st.device, st._stream(), err, 256)
+    _phase_rc(rc, "first_split", err.value.decode(errors="replace"))
+    return st
+
+
+def compute_distances(st: HullState) -> None:
+    """hull::compute_distances (hull.cpp:160-180)."""
+    _phase_rc(_lib.load().sh_b200_compute_distances(ctypes.byref(st._s), st.device, st._stream()),
+              "compute_distances")
+
+
+class FarthestList(collections.abc.Sequence):
+    """find_farthest's result: the device array (passed on to split_segments
+    as is) and, on first access, its host copy as SegmentMax items."""
+
+    def __init__(self, buf, m: int):
+        self.buf, self.m, self._items = buf, m, None
+
+    def _get(self):
+        if self._items is None:
+            raw = self.buf[:24 * self.m].cpu().numpy().tobytes()
+            a = (_lib.sh_segment_max * self.m).from_buffer_copy(raw) if self.m else []
+            self._items = [SegmentMax(int(e.key), float(e.value), int(e.index)) for e in a]
+        return self._items
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __len__(self):
+        return self.m
+
+
+def find_farthest(st: HullState) -> FarthestList:
+    """hull::find_farthest (hull.cpp:182-184; primitives.cpp:108-136)."""
+    import torch
+    cap = max(st.n, 1)
+    buf = torch.empty(24 * cap, dtype=torch.uint8, device=f"cuda:{st.device}")
+    m = ctypes.c_uint64(0)
+    rc = _lib.load().sh_b200_find_farthest(ctypes.byref(st._s), buf.data_ptr(), cap,
+                                           ctypes.byref(m), st.device, st._stream())
+    _phase_rc(rc, "find_farthest")
+    return FarthestList(buf, int(m.value))
+
+
+def split_segments(st: HullState, farthest) -> None:
+    """hull::split_segments (hull.cpp:186-194): ``farthest`` is find_farthest's
+    result or any sequence of SegmentMax."""
+    import torch
+    if isinstance(farthest, FarthestList):
+        buf, m = farthest.buf, farthest.m
+    else:
+        m = len(farthest)
+        arr = (_lib.sh_segment_max * max(m, 1))()
+        for j, e in enumerate(farthest):
+            arr[j].key, arr[j].value, arr[j].index = int(e.key), float(e.value), int(e.index)
+        buf = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(f"cuda:{st.device}")
+    rc = _lib.load().sh_b200_split_segments(ctypes.byref(st._s), buf.data_ptr(), m, st.device,
+                                            st._stream())
+    _phase_rc(rc, "split_segments")
+
+
+def mark_interior(st: HullState) -> None:
+    """hull::mark_interior (hull.cpp:196-201)."""
+    _phase_rc(_lib.load().sh_b200_mark_interior(ctypes.byref(st._s), st.device, st._stream()),
+              "mark_interior")
+
+
+def compact(st: HullState) -> int:
+    """hull::compact (hull.cpp:203-217): returns the rows removed."""
+    removed = ctypes.c_uint64(0)
+    rc = _lib.load().sh_b200_compact(ctypes.byref(st._s), ctypes.byref(removed), st.device,
+                                     st._stream())
+    _phase_rc(rc, "compact")
+    return int(removed.value)
+
+
 def run(points: PointSet, mode: Mode = Mode.WithPreprocess,
         backend: Backend = Backend.B200) -> HullResult:
     """seghull::hull::run (hull.hpp:95) on the B200 backend."""

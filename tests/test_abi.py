@@ -85,7 +85,7 @@ def test_struct_layouts_match_header(tmp_path):
     assert ctypes.sizeof(_lib.sh_hull_request) == 64
     # every ctypes mirror against the C compiler's view of include/seghull_b200.h
     names = ["sh_round_stat", "sh_phase_ms", "sh_kernel_ms", "sh_hull_request", "sh_hull_result",
-             "sh_shard", "sh_multi_ms"]
+             "sh_shard", "sh_multi_ms", "sh_hull_state", "sh_segment_max"]
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include "seghull_b200.h"\nint main(void){\n' +
                    "".join(f'printf("%zu\\n", sizeof({n}));\n' for n in names) + "return 0;}\n")
