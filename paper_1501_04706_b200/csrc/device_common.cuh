@@ -575,7 +575,12 @@ template <int T, int NS, bool IDS, int AUX, int NCW>
 SH_DEV uint32_t stream_prefetch(TileRing<T, NS, IDS, AUX, NCW>& R, uint32_t n, const double* X,
                                 const double* Y, const uint32_t* I, bool reverse, bool with_aux) {
   const TileWalk<T> w(n, reverse);
-  const uint32_t pre = min(w.mine, (uint32_t)NS);
+#ifndef SHB_PREFETCH
+#define SHB_PREFETCH 16
+#endif
+  // stages started before griddepcontrol.wait: they overlap the wait, but a
+  // full ring also queues ahead of the partials the prologue must read next
+  const uint32_t pre = min(w.mine, (uint32_t)min(NS, SHB_PREFETCH));
   if ((int)(threadIdx.x >> 5) == NCW && (threadIdx.x & 31) == 0) {
     for (uint32_t k = 0; k < pre; ++k) {
       const uint32_t first = w.first(k);

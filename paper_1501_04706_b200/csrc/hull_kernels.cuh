@@ -87,6 +87,11 @@ constexpr uint32_t TAIL_M = 4096;    // live sets up to this size finish in one 
 constexpr int STATS_CAP = 1 << 16;
 constexpr int STATS_EAGER = 64;      // stats read back together with the control block
 constexpr int MAX_ROUND_BLOCKS = 1024;
+// debug probes (Ctl::tl_round == 255): Bufs::dbg[DBG_SLOTS]; [0, 1024) relative
+// times written by the kernels, [DBG_RAW, DBG_SLOTS) raw %globaltimer values:
+//   1024 + b K1 CTA end | 1200 + b K2 CTA end | 1400 + b K3 CTA stream end (all warps)
+//   1600/1601 K2 CTA 0 entry / past griddepcontrol.wait, 1602/1603 K3, 1604/1605 KR
+constexpr int DBG_SLOTS = 2048, DBG_RAW = 1024;
 constexpr int MAX_RUNS = MAX_ROUND_BLOCKS;
 constexpr int RCWARPS = RTPB / 32 - 1;  // round kernel: consumer warps (+ 1 producer warp)
 constexpr int RCTHREADS = 32 * RCWARPS;
@@ -219,7 +224,7 @@ struct Bufs {
   StatRec* stats;
   unsigned long long* tile_status;
   uint32_t* blk_cnt;      // [2 * MAX_ROUND_BLOCKS] per-CTA counts of a large table scan
-  unsigned long long* dbg;  // [MAX_ROUND_BLOCKS] debug: per-CTA point-phase end of the traced round
+  unsigned long long* dbg;  // [DBG_SLOTS] debug probes (see DBG_SLOTS)
   // classification bits
   uint4* bits;
   // live set (runs)

@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(Cfg1::TPB, 1) k1_extremes(Bufs B) {
   // this CTA's extremes -> its partial (the next kernel combines them)
   K1Partial* part = B.k1part + blockIdx.x;
   cta_extremes(e, bad, part->e, &part->bad);
+  if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[1024 + blockIdx.x] = globaltimer_ns();
 }
 
 // ===========================================================================
@@ -349,7 +350,10 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   __syncthreads();
   // the points do not depend on K1: start the ring before waiting for it
   const uint32_t pre = stream_prefetch(R, B.n, B.in_x, B.in_y, B.in_id, SHB_K2_REVERSE != 0, true);
+  const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u;
+  if (probe) B.dbg[1600] = globaltimer_ns();
   pdl_wait();               // K1's partial extremes are complete and visible
+  if (probe) B.dbg[1601] = globaltimer_ns();
   pdl_launch_dependents();  // K3 may be scheduled on SMs this kernel frees
   // ---- every CTA combines K1's per-CTA extremes (no serial last-CTA step) ----
   __shared__ Fin s_fin;
@@ -562,6 +566,7 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
       part->kept = s_kb;
       part->noncol = s_nc;
       if (blockIdx.x == 0) c->mark[2] = globaltimer_ns() - c->t0_ns;
+      if (c->tl_round == 255u) B.dbg[1200 + blockIdx.x] = globaltimer_ns();
     }
   }
 }

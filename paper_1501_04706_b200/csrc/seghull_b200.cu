@@ -85,12 +85,23 @@ std::vector<size_t> g_dev_mem;  // HBM bytes per device (same lifetime and lock 
 // hulls): pinned chunks + one event each.  Owned by a workspace, so every
 // call -- and every host thread of a multi-GPU call -- has its own ring on
 // its own device: no shared host state, no lock held across a copy.
-constexpr size_t H2D_CHUNK = 8u << 20;
-constexpr int H2D_NBUF = 4;
+constexpr size_t H2D_CHUNK = 8u << 20;  // default chunk (SHB_H2D_CHUNK_MB)
+constexpr int H2D_NBUF = 4;             // default chunks in flight (SHB_H2D_NBUF)
+constexpr int H2D_MAXBUF = 8;
 struct PinnedRing {
-  char* buf[H2D_NBUF] = {};
-  cudaEvent_t done[H2D_NBUF] = {};
+  char* buf[H2D_MAXBUF] = {};
+  cudaEvent_t done[H2D_MAXBUF] = {};
+  size_t chunk = H2D_CHUNK;
+  int nbuf = 0;      // 0: not allocated yet
+  int threads = 8;   // host threads packing / unpacking a chunk
 };
+
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  if (!e) return dflt;
+  const int v = std::atoi(e);
+  return v < lo ? lo : v > hi ? hi : v;
+}
 
 struct Workspace {
   int device = 0;
@@ -115,7 +126,7 @@ struct Workspace {
     cudaGetDevice(&cur);
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);  // nothing of ours may still be in flight
-    for (int b = 0; b < H2D_NBUF; ++b) {
+    for (int b = 0; b < H2D_MAXBUF; ++b) {
       if (ring.done[b]) cudaEventSynchronize(ring.done[b]);
       if (ring.done[b]) cudaEventDestroy(ring.done[b]);
       if (ring.buf[b]) cudaFreeHost(ring.buf[b]);
@@ -227,7 +238,7 @@ std::unique_ptr<Workspace> make_workspace(int device, uint64_t n_cap, uint64_t s
   const size_t o_k1 = take(sizeof(K1Partial) * ws->stream_grid);
   const size_t o_k2 = take(sizeof(K2Partial) * ws->stream_grid);
   const size_t o_blk = take(sizeof(uint32_t) * 2 * MAX_ROUND_BLOCKS);
-  const size_t o_dbg = take(sizeof(unsigned long long) * MAX_ROUND_BLOCKS);
+  const size_t o_dbg = take(sizeof(unsigned long long) * DBG_SLOTS);
   const size_t o_tiles = take(sizeof(unsigned long long) * ws->tiles_cap);
   const size_t o_bits = take(sizeof(uint4) * ((N + 63) / 64));
   size_t o_lxy[2], o_lis[2], o_rc[2], o_tx[2], o_ty[2], o_tid[2], o_sd[3], o_sw[3];
@@ -379,18 +390,23 @@ struct RunOut {
 };
 
 void ensure_ring(Workspace& ws) {
-  if (ws.ring.buf[0]) return;
-  for (int b = 0; b < H2D_NBUF; ++b) {
-    CK(cudaMallocHost((void**)&ws.ring.buf[b], H2D_CHUNK));
-    CK(cudaEventCreateWithFlags(&ws.ring.done[b], cudaEventDisableTiming));
+  PinnedRing& R = ws.ring;
+  if (R.nbuf) return;
+  R.chunk = (size_t)env_int("SHB_H2D_CHUNK_MB", (int)(H2D_CHUNK >> 20), 1, 64) << 20;
+  const int nb = env_int("SHB_H2D_NBUF", H2D_NBUF, 2, H2D_MAXBUF);
+  R.threads = env_int("SHB_H2D_THREADS", 8, 1, 64);
+  for (int b = 0; b < nb; ++b) {
+    CK(cudaMallocHost((void**)&R.buf[b], R.chunk));
+    CK(cudaEventCreateWithFlags(&R.done[b], cudaEventDisableTiming));
   }
+  R.nbuf = nb;
 }
 
 // Host -> device copy of a caller's buffer.  Pinned (or registered) memory
 // goes straight to the copy engine.  Pageable memory would be staged by the
 // driver through one bounce buffer at ~11 GB/s; instead it is packed into the
 // workspace's pinned chunks by the host cores (OpenMP) and each chunk is
-// copied while the next ones are packed (H2D_NBUF chunks in flight).
+// copied while the next ones are packed (nbuf chunks in flight).
 void h2d_or_copy(Workspace& ws, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
                  bool host, cudaStream_t st) {
   if (!host || bytes < (H2D_CHUNK >> 2)) {
@@ -407,13 +423,14 @@ void h2d_or_copy(Workspace& ws, void* dst, const void* src, size_t bytes, cudaMe
   PinnedRing& R = ws.ring;
   const char* s = (const char*)src;
   char* d = (char*)dst;
-  for (size_t off = 0, k = 0; off < bytes; off += H2D_CHUNK, ++k) {
-    const int b = (int)(k % H2D_NBUF);
-    const size_t len = std::min(H2D_CHUNK, bytes - off);
+  const int nt = R.threads;
+  for (size_t off = 0, k = 0; off < bytes; off += R.chunk, ++k) {
+    const int b = (int)(k % R.nbuf);
+    const size_t len = std::min(R.chunk, bytes - off);
     CK(cudaEventSynchronize(R.done[b]));  // every earlier copy out of / into buf[b] finished
     char* pb = R.buf[b];
-    const long parts = 16;
-#pragma omp parallel for num_threads(8) schedule(static)
+    const long parts = 2 * nt;
+#pragma omp parallel for num_threads(nt) schedule(static)
     for (long t = 0; t < parts; ++t) {
       const size_t a = len * t / parts, e = len * (t + 1) / parts;
       std::memcpy(pb + a, s + off + a, e - a);
@@ -430,29 +447,30 @@ void h2d_or_copy(Workspace& ws, void* dst, const void* src, size_t bytes, cudaMe
 // id_base).  Synchronous: the caller's array is complete on return.
 void d2h_ring(Workspace& ws, void* dst, const void* src, size_t n, bool widen, uint64_t id_base,
               cudaStream_t st) {
-  const size_t esz = widen ? 4 : 8;  // source element size
-  const size_t per = H2D_CHUNK / esz;  // elements per chunk
-  const size_t nchunks = (n + per - 1) / per;
   ensure_ring(ws);
   PinnedRing& R = ws.ring;
+  const size_t esz = widen ? 4 : 8;  // source element size
+  const size_t per = R.chunk / esz;  // elements per chunk
+  const size_t nchunks = (n + per - 1) / per;
+  const int nt = R.threads;
   const char* s = (const char*)src;
   auto issue = [&](size_t k) {
-    const int b = (int)(k % H2D_NBUF);
+    const int b = (int)(k % R.nbuf);
     const size_t len = std::min(per, n - k * per) * esz;
     CK(cudaEventSynchronize(R.done[b]));  // an earlier H2D out of buf[b] may still run
     CK(cudaMemcpyAsync(R.buf[b], s + k * per * esz, len, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(R.done[b], st));
   };
-  for (size_t k = 0; k < nchunks && k < (size_t)H2D_NBUF; ++k) issue(k);
+  for (size_t k = 0; k < nchunks && k < (size_t)R.nbuf; ++k) issue(k);
   for (size_t k = 0; k < nchunks; ++k) {
-    const int b = (int)(k % H2D_NBUF);
+    const int b = (int)(k % R.nbuf);
     CK(cudaEventSynchronize(R.done[b]));
     const size_t e0 = k * per, cnt = std::min(per, n - e0);
-    const long parts = 16;
+    const long parts = 2 * nt;
     if (widen) {
       const uint32_t* pb = (const uint32_t*)R.buf[b];
       int64_t* d = (int64_t*)dst + e0;
-#pragma omp parallel for num_threads(8) schedule(static)
+#pragma omp parallel for num_threads(nt) schedule(static)
       for (long t = 0; t < parts; ++t) {
         const size_t a = cnt * t / parts, e = cnt * (t + 1) / parts;
         for (size_t i = a; i < e; ++i) d[i] = (int64_t)(pb[i] + id_base);
@@ -460,13 +478,13 @@ void d2h_ring(Workspace& ws, void* dst, const void* src, size_t n, bool widen, u
     } else {
       const char* pb = R.buf[b];
       char* d = (char*)dst + e0 * 8;
-#pragma omp parallel for num_threads(8) schedule(static)
+#pragma omp parallel for num_threads(nt) schedule(static)
       for (long t = 0; t < parts; ++t) {
         const size_t a = cnt * 8 * t / parts, e = cnt * 8 * (t + 1) / parts;
         std::memcpy(d + a, pb + a, e - a);
       }
     }
-    if (k + H2D_NBUF < nchunks) issue(k + H2D_NBUF);
+    if (k + R.nbuf < nchunks) issue(k + R.nbuf);
   }
 }
 
@@ -575,9 +593,11 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
     for (int i = 0; i < 8; ++i) g_last_tl[i + 1] = c.mark[i];
   }
   if (g_trace_round) {
-    g_last_ctas.resize(MAX_ROUND_BLOCKS);
-    CK(cudaMemcpy(g_last_ctas.data(), B.dbg, sizeof(unsigned long long) * MAX_ROUND_BLOCKS,
+    g_last_ctas.resize(DBG_SLOTS);
+    CK(cudaMemcpy(g_last_ctas.data(), B.dbg, sizeof(unsigned long long) * DBG_SLOTS,
                   cudaMemcpyDeviceToHost));
+    for (int i = DBG_RAW; i < DBG_SLOTS; ++i)  // raw %globaltimer probes -> since K1 start
+      if (g_last_ctas[i]) g_last_ctas[i] -= c.t0_ns;
   }
   out.rounds = c.round;
   out.kept = rq.mode == SH_MODE_WITH_PREPROCESS ? c.kept : n;

@@ -41,8 +41,8 @@ for _ in range(reps):
             print("   kernel marks (us): K1 end %.1f | K2 start %.1f end %.1f | K3 start %.1f end %.1f | KR start %.1f end %.1f" % tuple(ts[0:7]))
         else:
             print(f"   trace round {trace} (us since K1 start: start, table, prefix, points, flush, barrier, [winner]):", [round(t, 2) for t in ts])
-        cb = (ctypes.c_ulonglong * 1024)()
-        L.sh_b200_debug_last_ctas(cb, 1024)
+        cb = (ctypes.c_ulonglong * 2048)()
+        L.sh_b200_debug_last_ctas(cb, 2048)
         if trace == 255:
             import statistics
             for name, off in (("K1", 0), ("K2", 256), ("K3", 512)):
@@ -50,8 +50,13 @@ for _ in range(reps):
                 if e:
                     print(f"   {name} CTA stream ends: min {e[0]:.1f} median {statistics.median(e):.1f} "
                           f"p90 {e[int(len(e) * 0.9)]:.1f} max {e[-1]:.1f} us", flush=True)
-            print("   K1 last CTA (us): ticket won, fence, combined, reduced, finalized:",
-                  [round(cb[768 + k] / 1e3, 1) for k in range(8)], flush=True)
+            for name, off in (("K1 end", 1024), ("K2 end", 1200), ("K3 streams (all warps)", 1400)):
+                e = sorted(cb[off + i] / 1e3 for i in range(148) if cb[off + i])
+                if e:
+                    print(f"   {name}: min {e[0]:.1f} median {statistics.median(e):.1f} "
+                          f"p90 {e[int(len(e) * 0.9)]:.1f} max {e[-1]:.1f} us", flush=True)
+            print("   CTA0 entry/past-wait (us): K2 %.1f/%.1f K3 %.1f/%.1f KR %.1f/%.1f"
+                  % tuple(cb[1600 + k] / 1e3 for k in range(6)), flush=True)
             continue
         ends = sorted(cb[i] / 1e3 for i in range(1024) if cb[i])
         slow = sorted((cb[i] / 1e3, i) for i in range(1024) if cb[i])[-10:]
