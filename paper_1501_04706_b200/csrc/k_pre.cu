@@ -313,13 +313,17 @@ SH_DEV void combine_k1(const Bufs& B, Fin& s_fin, bool publish) {
   }
   __shared__ ExtRec s_ext[4];
   __shared__ unsigned long long s_bad;
+  const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u;
+  if (probe) B.dbg[1608] = globaltimer_ns() + (unsigned long long)(e[0].x == -1.0);
   cta_extremes(e, bad, s_ext, &s_bad);
   __syncthreads();
+  if (probe) B.dbg[1609] = globaltimer_ns();
   if (threadIdx.x == 0) {
     const ExtRec ee[4] = {s_ext[0], s_ext[1], s_ext[2], s_ext[3]};
     compute_fin(s_fin, ee, s_bad);
     if (publish && blockIdx.x == 0) {
       write_fin(c, s_fin);
+      if (c->tl_round == 255u) B.dbg[1610] = globaltimer_ns();
       const unsigned long long now = globaltimer_ns() - c->t0_ns;
       c->mark[0] = now;
       c->mark[1] = now;

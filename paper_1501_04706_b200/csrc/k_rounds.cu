@@ -250,7 +250,10 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   // the points do not depend on K2 (their class bits do): start the ring on
   // them before waiting; the bits follow once K2 is complete
   const uint32_t pre = stream_prefetch(R, B.n, B.in_x, B.in_y, B.in_id, false, false);
+  const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u;
+  if (probe) B.dbg[1602] = globaltimer_ns();
   pdl_wait();               // K2's classes and partials are complete and visible
+  if (probe) B.dbg[1603] = globaltimer_ns();
   pdl_launch_dependents();  // the round kernel may be scheduled on SMs this kernel frees
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) {
     stream_drain_points(R, pre, B.n, reinterpret_cast<const unsigned char*>(B.bits));
@@ -295,9 +298,17 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
       s_kept = 0;
       s_nc = 0;
     }
+    if (probe) B.dbg[1606] = globaltimer_ns() + ((key[0][0] ^ kb) == 1ull ? 1ull : 0ull);
     cta_lexmin<2, 4>(key, valid, s_best2, win);  // starts with a barrier
-    if (kb) atomicAdd(&s_kept, kb);
-    if (nc) s_nc = 1u;
+    if (probe) B.dbg[1607] = globaltimer_ns();
+    {  // one shared atomic per warp (threads past the grid hold zeros)
+      unsigned long long wk = kb;
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) wk += __shfl_xor_sync(FULL, wk, m);
+      const bool wnc = __any_sync(FULL, nc != 0);
+      if (lane == 0 && wk) atomicAdd(&s_kept, wk);
+      if (lane == 0 && wnc) s_nc = 1u;
+    }
     if (win[0]) s_cand[0] = a[0];
     if (win[1]) s_cand[1] = a[1];
     __syncthreads();
@@ -469,6 +480,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
 
   // ---- flush the CTA's records to the global slots of round 2's argmax ----
   __syncthreads();
+  if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[1400 + blockIdx.x] = globaltimer_ns();
   if (threadIdx.x == 0 && (s_off & 1u) && s_off < B.run_q) {  // pad the run to an even length
     Oxy[run_base + s_off] = make_double2(0.0, 0.0);
     Ois[run_base + s_off] = make_uint2(NONE, NONE);
@@ -486,30 +498,42 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&c->ticket, 1u) == gridDim.x - 1;
   __syncthreads();
+  // the last CTA combines the CTAs' rows: one thread per row, every field
+  // loaded in one round trip, run counts summed per warp
   if (!s_last) return;
+  const bool probe_c = threadIdx.x == 0 && c->tl_round == 255u;
+  if (probe_c) B.dbg[1611] = globaltimer_ns();
   __threadfence();
-  const uint32_t mn = sum_runs(B.run_cnt[1], gridDim.x, s_ws);
+  __shared__ uint32_t s_mn;
   {  // the farthest record of each segment over the CTAs' rows -> Srec[1]
     __shared__ unsigned long long s_best4[4][4];
     Cand a[4];
     unsigned long long key[4][4];
     bool valid[4], win[4];
+    const bool row = threadIdx.x < gridDim.x;
+    const uint32_t rc = row ? __ldcg(B.run_cnt[1] + threadIdx.x) : 0u;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < 4; ++t) {  // every field in one round trip
       a[t] = empty_cand();
-      if (threadIdx.x < gridDim.x) {
+      if (row) {
         const SlotRec* q = B.Rc[1] + (size_t)threadIdx.x * NSLOT + t;
         a[t].id = __ldcg(&q->id);
-        if (a[t].id != NONE) {
-          a[t].d = __ldcg(&q->d);
-          a[t].x = __ldcg(&q->x);
-          a[t].y = __ldcg(&q->y);
-        }
+        a[t].d = __ldcg(&q->d);
+        a[t].x = __ldcg(&q->x);
+        a[t].y = __ldcg(&q->y);
       }
+    }
+    if (threadIdx.x == 0) s_mn = 0;
+    const uint32_t wsum = __reduce_add_sync(FULL, rc);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
       a[t].pos = 0;
       cand_keys(a[t], (uint32_t)t < Slon, key[t]);
       valid[t] = a[t].id != NONE;
     }
+    __syncthreads();
+    if (lane == 0 && wsum) atomicAdd(&s_mn, wsum);
+    if (probe_c) B.dbg[1612] = globaltimer_ns();
     cta_lexmin<4, 4>(key, valid, s_best4, win);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -522,6 +546,8 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
     }
   }
   if (threadIdx.x != 0) return;
+  const uint32_t mn = s_mn;
+  if (probe_c) B.dbg[1613] = globaltimer_ns();
   c->ticket = 0;
   const uint32_t before = c->S_cur + c->m_cur;
   StatRec st;
@@ -1141,7 +1167,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   __shared__ uint32_t s_off, s_coff;
   __shared__ uint32_t s_pref[MAX_RUNS + 1];
   Ctl* c = B.ctl;
+  const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u;
+  if (probe) B.dbg[1604] = globaltimer_ns();
   pdl_wait();  // round 1 (K3) is complete and visible
+  if (probe) B.dbg[1605] = globaltimer_ns();
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   uint32_t r = *(volatile uint32_t*)&c->round + 1;
   const uint32_t trace_r = c->tl_round;  // debug timeline of CTA 0 in this round (0: off)

@@ -57,6 +57,10 @@ for _ in range(reps):
                           f"p90 {e[int(len(e) * 0.9)]:.1f} max {e[-1]:.1f} us", flush=True)
             print("   CTA0 entry/past-wait (us): K2 %.1f/%.1f K3 %.1f/%.1f KR %.1f/%.1f"
                   % tuple(cb[1600 + k] / 1e3 for k in range(6)), flush=True)
+            print("   K3 CTA0 partials loaded %.1f, lexmin done %.1f | K2 CTA0 K1-partials loaded %.1f, "
+                  "extremes done %.1f, fin written %.1f | K3 close: ticket %.1f runs summed %.1f rows combined %.1f"
+                  % tuple(cb[1606 + k] / 1e3 for k in range(8)),
+                  flush=True)
             continue
         ends = sorted(cb[i] / 1e3 for i in range(1024) if cb[i])
         slow = sorted((cb[i] / 1e3, i) for i in range(1024) if cb[i])[-10:]
