@@ -65,8 +65,9 @@ enum sh_flags {
                           /* the vertices never leave HBM (shard hulls -> gather)    */
   SH_OUT_PAD = 16u        /* with SH_OUT_DEVICE: write ONE fixed-size payload block  */
                           /* at out_x: {x f64[cap] | y f64[cap] | index i64[cap]},   */
-                          /* vertices then copies of vertex 0; h > cap writes NaN x  */
-                          /* and h into index[0] (see sh_b200_hull_gathered)         */
+                          /* the h vertices, then padding (copies of vertex 0 with   */
+                          /* index -1); h > cap writes NaN x and h into index[0]     */
+                          /* (see sh_b200_hull_gathered)                             */
 };
 
 /* hull.hpp:35-40 SegmentStats, plus the device time at which the round ended */
@@ -198,7 +199,8 @@ int sh_b200_hull_shards(const sh_shard* shards, int nshards, int mode, uint32_t 
 /* The merge step alone, for one-process-per-GPU callers (torch.distributed):
  * `payload` = nblocks gathered SH_OUT_PAD blocks of block_cap vertices each
  * (device memory on `device`, e.g. the output of one all-gather); n_total =
- * points in the whole input.  Returns SH_CAP_TOO_SMALL with *out_h = the
+ * points in the whole input.  Padding (index -1) is dropped on the device
+ * before the merge hull, whose input is the real vertices only.  Returns SH_CAP_TOO_SMALL with *out_h = the
  * block capacity needed when a block carries the overflow marker.           */
 int sh_b200_hull_gathered(const double* payload, uint32_t nblocks, uint64_t block_cap,
                           uint64_t n_total, int mode, uint32_t flags, int device, void* stream,

@@ -214,6 +214,8 @@ struct Bufs {
   const double* in_y;
   const uint32_t* in_id;  // may be null: id == position
   uint32_t n;
+  const uint32_t* n_dev;  // small path only, may be null: the real point count is
+                          // *n_dev <= n, written on the device by an earlier kernel
   uint32_t s_cap;
   // control
   Ctl* ctl;

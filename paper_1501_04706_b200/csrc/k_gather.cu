@@ -10,10 +10,16 @@
 //              GPU stores its hull straight into the root's gather buffer.
 //              A hull with h > cap writes NaN x and h into index[0]: the merge
 //              then reports SH_CAP_TOO_SMALL with the capacity it needs.
-//   k_unpack   R gathered blocks -> the merge hull's SoA input x[], y[] and
-//              u32 ids (global input indices; they break ties and become the
-//              output indices, so the merged hull carries canonical GLOBAL
-//              indices exactly as the whole-input run would).
+//              Pad entries carry index -1, so the merge can drop them: thousands
+//              of exact copies of one vertex would all tie for the farthest
+//              point and serialise on its record (8 x 2048 padded vertices took
+//              1.75 ms to merge, the ~450 real ones take ~40 us).
+//   k_count /  R gathered blocks -> the merge hull's SoA input x[], y[] and
+//   k_unpack   u32 ids of the REAL vertices only (global input indices; they
+//              break ties and become the output indices, so the merged hull
+//              carries canonical GLOBAL indices exactly as the whole-input run
+//              would).  An overflow block (NaN x) is copied whole, so the merge
+//              reports it.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -76,23 +82,58 @@ __global__ void k5_pack(Bufs B, double* blk, uint64_t cap, unsigned long long id
     if (i < h) vert((uint32_t)i, x, y, id);
     ox[i] = x;
     oy[i] = y;
-    oi[i] = (long long)(id_base + id);
+    oi[i] = i < h ? (long long)(id_base + id) : -1ll;  // -1: padding
   }
 }
 
-// blocks [R][3][cap] -> x[R*cap], y[R*cap], ids[R*cap]
+// per block: its entries to keep (the real vertices, or every entry of an
+// overflow block) -> cnt[b]; one CTA per block
+__global__ void k_count(const double* __restrict__ pay, uint64_t cap, uint32_t* cnt) {
+  const double* blk = pay + (uint64_t)blockIdx.x * 3 * cap;
+  const long long* idx = reinterpret_cast<const long long*>(blk + 2 * cap);
+  const bool overflow = blk[0] != blk[0];  // NaN marker
+  uint32_t c = 0;
+  for (uint64_t k = threadIdx.x; k < cap; k += blockDim.x) c += (overflow || idx[k] >= 0) ? 1u : 0u;
+  c = __reduce_add_sync(FULL, c);
+  __shared__ uint32_t s_c;
+  if (threadIdx.x == 0) s_c = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_c, c);
+  __syncthreads();
+  if (threadIdx.x == 0) cnt[blockIdx.x] = s_c;
+}
+
+// kept entries of block b -> [sum of cnt[< b], ...): x, y, u32 ids; the total
+// goes to cnt[R] (block 0)
 __global__ void k_unpack(const double* __restrict__ pay, uint32_t R, uint64_t cap,
-                         double* __restrict__ x, double* __restrict__ y,
-                         uint32_t* __restrict__ ids) {
-  const uint64_t total = (uint64_t)R * cap;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
-    const uint64_t b = i / cap, k = i - b * cap;
-    const double* blk = pay + b * 3 * cap;
-    x[i] = blk[k];
-    y[i] = blk[cap + k];
-    ids[i] = (uint32_t) reinterpret_cast<const long long*>(blk + 2 * cap)[k];
+                         uint32_t* __restrict__ cnt, double* __restrict__ x,
+                         double* __restrict__ y, uint32_t* __restrict__ ids) {
+  __shared__ uint32_t s_base, s_tot;
+  if (threadIdx.x == 0) s_base = s_tot = 0;
+  __syncthreads();
+  uint32_t base = 0, tot = 0;
+  for (uint32_t b = threadIdx.x; b < R; b += blockDim.x) {
+    const uint32_t v = cnt[b];
+    tot += v;
+    if (b < blockIdx.x) base += v;
   }
+  base = __reduce_add_sync(FULL, base);
+  tot = __reduce_add_sync(FULL, tot);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_base, base);
+    atomicAdd(&s_tot, tot);
+  }
+  __syncthreads();
+  const double* blk = pay + (uint64_t)blockIdx.x * 3 * cap;
+  const long long* idx = reinterpret_cast<const long long*>(blk + 2 * cap);
+  const uint32_t keep = cnt[blockIdx.x];  // real vertices are the block's prefix
+  for (uint32_t k = threadIdx.x; k < keep; k += blockDim.x) {
+    const uint32_t o = s_base + k;
+    x[o] = blk[k];
+    y[o] = blk[cap + k];
+    ids[o] = (uint32_t)idx[k];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[R] = s_tot;
 }
 
 void launch_k5_pack(const Bufs& B, double* blk, uint64_t cap, unsigned long long id_base,
@@ -110,11 +151,11 @@ void launch_k5_pack(const Bufs& B, double* blk, uint64_t cap, unsigned long long
   cudaLaunchKernelEx(&cfg, k5_pack, B, blk, cap, id_base);
 }
 
-void launch_unpack(const double* pay, uint32_t R, uint64_t cap, double* x, double* y,
-                   uint32_t* ids, cudaStream_t s) {
-  const uint64_t total = (uint64_t)R * cap;
-  const int grid = (int)(total / 256 + 1 < 148 * 4 ? total / 256 + 1 : 148 * 4);
-  k_unpack<<<grid, 256, 0, s>>>(pay, R, cap, x, y, ids);
+// cnt: R + 1 words of device scratch; cnt[R] = points of the merge input
+void launch_unpack(const double* pay, uint32_t R, uint64_t cap, uint32_t* cnt, double* x,
+                   double* y, uint32_t* ids, cudaStream_t s) {
+  k_count<<<R, 256, 0, s>>>(pay, cap, cnt);
+  k_unpack<<<R, 256, 0, s>>>(pay, R, cap, cnt, x, y, ids);
 }
 
 }  // namespace shb

@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
 template <bool FILTER, bool IDS>
 __global__ void __launch_bounds__(1024, 1) k_small_pre(Bufs B) {
   Ctl* c = B.ctl;
-  const uint32_t n = B.n;
+  const uint32_t n = B.n_dev ? *B.n_dev : B.n;  // the merge input's count is device-written
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* __restrict__ X = B.in_x;
   const double* __restrict__ Y = B.in_y;

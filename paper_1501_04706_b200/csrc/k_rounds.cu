@@ -227,7 +227,11 @@ constexpr int K3_NP = 2 * Cfg3::CH;   // points per consumer thread per tile
 
 template <bool IDS>
 struct K3Layout {
-  using Ring = TileRing<Cfg3::T, Cfg3::NS, IDS, 16, Cfg3::CW>;
+#ifndef SHB_K3_NS_IDS
+#define SHB_K3_NS_IDS SHB_K3_NS
+#endif
+  // with caller ids each point carries 4 more bytes: the ring may need fewer stages
+  using Ring = TileRing<Cfg3::T, IDS ? SHB_K3_NS_IDS : Cfg3::NS, IDS, 16, Cfg3::CW>;
   static constexpr size_t kRing = (Ring::kBytes + 127) / 128 * 128;
   static constexpr size_t kBytes = kRing;
 };

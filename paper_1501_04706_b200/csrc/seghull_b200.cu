@@ -47,8 +47,8 @@ void launch_preprocess(const Bufs& B, double* ox, double* oy, unsigned long long
                        cudaStream_t s);
 void launch_k5_pack(const Bufs& B, double* blk, uint64_t cap, unsigned long long id_base,
                     cudaStream_t s);
-void launch_unpack(const double* pay, uint32_t R, uint64_t cap, double* x, double* y,
-                   uint32_t* ids, cudaStream_t s);
+void launch_unpack(const double* pay, uint32_t R, uint64_t cap, uint32_t* cnt, double* x,
+                   double* y, uint32_t* ids, cudaStream_t s);
 }  // namespace shb
 
 using namespace shb;
@@ -492,7 +492,7 @@ void d2h_ring(Workspace& ws, void* dst, const void* src, size_t n, bool widen, u
 // K1, K2, K3, the cooperative round kernel, K5 (device outputs), and the
 // read-back of the control block + the first STATS_EAGER round stats.
 RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& res,
-                    cudaStream_t st, bool timings) {
+                    cudaStream_t st, bool timings, const uint32_t* n_dev = nullptr) {
   RunOut out;
   Bufs B = ws.B;
   const uint64_t n = rq.n;
@@ -522,6 +522,7 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   }
   if (timings) CK(cudaEventRecord(ws.ev[1], st));
   B.n = (uint32_t)n;
+  B.n_dev = n <= SMALL_N ? n_dev : nullptr;
   const bool ids = B.in_id != nullptr;
 
   // a zeroed control block is the initial state (ST_RUNNING == 0)
@@ -634,8 +635,10 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
 // One hull on one device.  `keep`: on success the workspace is handed back to
 // the caller instead of the pool (the multi-GPU path re-packs from its final
 // head table when a shard hull outgrew the payload).
+// n_dev (internal, the shard merge): the real point count lives on the device
+// (<= rq->n, which bounds it and sizes the grids); small inputs only.
 int hull_impl(const sh_hull_request* rq, sh_hull_result* res,
-              std::unique_ptr<Workspace>* keep = nullptr) {
+              std::unique_ptr<Workspace>* keep = nullptr, const uint32_t* n_dev = nullptr) {
   if (!rq || !res) return SH_INVALID_ARGUMENT;
   res->h = 0;
   res->rounds = 0;
@@ -667,14 +670,14 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res,
     ws = acquire(rq->device, n);
     const bool timings = (rq->flags & SH_PHASE_TIMINGS) != 0;
     cudaStream_t st = rq->stream ? (cudaStream_t)rq->stream : ws->stream;
-    RunOut o = run_pipeline(*ws, *rq, *res, st, timings);
+    RunOut o = run_pipeline(*ws, *rq, *res, st, timings, n_dev);
     if (o.code == -1) {  // segment tables or live sets too small: regrow to the worst case, rerun
       const int dev = ws->device;
       const uint64_t cap = std::max<uint64_t>(n, 1u << 12);
       ws.reset();  // synchronises its stream before freeing anything
       ws = make_workspace_retry(dev, cap, cap + 2, cap);
       st = rq->stream ? (cudaStream_t)rq->stream : ws->stream;  // the old pool stream is gone
-      o = run_pipeline(*ws, *rq, *res, st, timings);
+      o = run_pipeline(*ws, *rq, *res, st, timings, n_dev);
       if (o.code == -1) {
         o.code = SH_INTERNAL_ERROR;
         o.msg = "run: segment table overflow";
@@ -896,21 +899,35 @@ int gathered_impl(const double* pay, uint32_t R, uint64_t bcap, uint64_t n_total
     double* sx = (double*)ws->stage;
     double* sy = (double*)((char*)ws->stage + align_up(8 * ws->n_cap, 256));
     uint32_t* sid = (uint32_t*)((char*)ws->stage + 2 * align_up(8 * ws->n_cap, 256));
-    launch_unpack(pay, R, bcap, sx, sy, sid, st);
+    // per-block counts in the workspace's scan scratch (2 MAX_ROUND_BLOCKS words)
+    if (R + 1 > 2u * MAX_ROUND_BLOCKS) throw CudaFail{cudaErrorInvalidValue, "more than 2047 blocks"};
+    uint32_t* cnt = ws->B.blk_cnt;
+    launch_unpack(pay, R, bcap, cnt, sx, sy, sid, st);
     CK(cudaGetLastError());
+    // the merge input is the real vertices only; their count stays on the
+    // device for the one-CTA small path (no read-back), else it is read back
+    uint32_t mreal = (uint32_t)m;
+    const uint32_t* n_dev = nullptr;
+    if (m <= SMALL_N) {
+      n_dev = cnt + R;
+    } else {
+      CK(cudaMemcpyAsync(ws->h_res, cnt + R, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::memcpy(&mreal, ws->h_res, sizeof(mreal));
+    }
     sh_hull_request rq;
     std::memset(&rq, 0, sizeof(rq));
     rq.x = sx;
     rq.y = sy;
     rq.ids = sid;
-    rq.n = m;
+    rq.n = mreal;
     rq.mode = mode;
     rq.flags = SH_DEVICE_PTRS | (flags & (SH_OUT_DEVICE | SH_NO_STATS | SH_PHASE_TIMINGS));
     rq.device = device;
     rq.stream = st;
     // the staging arrays stay ours until the merge has read them
     std::unique_ptr<Workspace> hold = std::move(ws);
-    int rc = hull_impl(&rq, res);
+    int rc = hull_impl(&rq, res, nullptr, n_dev);
     if (rc == SH_NON_FINITE_INPUT) {  // a NaN marker: which block, what it needs
       uint64_t need = 0;
       for (uint32_t b = 0; b < R; ++b) {

@@ -34,7 +34,8 @@ def _free_port():
 
 def _pack_standin(x, y, block, *, first, mode, stream=None):
     """SH_OUT_PAD restated: {x[cap] | y[cap] | int64 global index[cap]}, vertices
-    then copies of vertex 0; h > cap -> NaN x and h in index[0]."""
+    then padding (copies of vertex 0 with index -1); h > cap -> NaN x and h in
+    index[0]."""
     cap = block.numel() // 3
     r = oracle.hull_run(x, y, mode)
     idx = oracle.canonical_index(x, y, r.x, r.y) + first
@@ -50,7 +51,8 @@ def _pack_standin(x, y, block, *, first, mode, stream=None):
     pad = lambda v: np.concatenate([v, np.full(cap - h, v[0], v.dtype)])
     bx.copy_(torch.from_numpy(pad(r.x)))
     by.copy_(torch.from_numpy(pad(r.y)))
-    bi.copy_(torch.from_numpy(pad(idx.astype(np.int64))))
+    bi.copy_(torch.from_numpy(np.concatenate([idx.astype(np.int64),
+                                              np.full(cap - h, -1, np.int64)])))
     return h
 
 
@@ -66,6 +68,8 @@ def _merge_standin(g, nblocks, n_total, mode, stream=None, out_device=True):
         need = [int(b[k, 2, :].contiguous().view(torch.int64)[0]) for k in range(nblocks)
                 if np.isnan(float(b[k, 0, 0]))]
         return None, max(need)
+    real = ids >= 0  # padding dropped
+    x, y, ids = x[real], y[real], ids[real]
     r = oracle.hull_run(x, y, mode)
     out = np.array([ids[(x == a) & (y == c)].min() for a, c in zip(r.x, r.y)], np.int64)
     return (r.x, r.y, out), r.x.size
