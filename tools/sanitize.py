@@ -23,3 +23,26 @@ for name, (x, y) in cases:
         ref = oracle.hull_run(x, y, mode)
         ok = np.array_equal(np.asarray(r.x), np.asarray(ref.x)) and np.array_equal(np.asarray(r.y), np.asarray(ref.y))
         print(f"{name} m{mode}: h={len(r)} rounds={r.rounds} {'ok' if ok else 'MISMATCH'}", flush=True)
+
+# the multi-GPU entry points (3 shards on this device: K5-pack into the gather
+# buffer, k_count / k_unpack, the merge) and the per-phase device API
+for name, (x, y) in [("multi uniform", dataio.gen_uniform(int(3e5 * k) + 3, 5)),
+                     ("multi circle", dataio.gen_circle(int(1e5 * k) + 3, 5))]:
+    m = hull.run_multi(x, y, [0, 0, 0], 1)
+    ref = oracle.hull_run(x, y, 1)
+    ok = np.array_equal(np.asarray(m.x), np.asarray(ref.x)) and np.array_equal(np.asarray(m.y), np.asarray(ref.y))
+    print(f"{name}: h={len(m)} {'ok' if ok else 'MISMATCH'}", flush=True)
+x, y = dataio.gen_uniform(5000, 9)
+st = hull.first_split(x, y)
+for _ in range(64):
+    hull.compute_distances(st)
+    far = hull.find_farthest(st)
+    if not any(f.value > 0.0 for f in far) and st.size() == len(far):
+        break
+    hull.split_segments(st, far)
+    hull.mark_interior(st)
+    hull.compact(st)
+ref = oracle.hull_run(x, y, 2)
+c = st.columns()
+ok = np.array_equal(c["x"], ref.x) and np.array_equal(c["y"], ref.y)
+print(f"phases uniform 5000: h={st.size()} {'ok' if ok else 'MISMATCH'}", flush=True)

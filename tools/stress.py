@@ -1,6 +1,9 @@
 """Randomised parity stress: many shapes and sizes, both modes, optional ids,
-host and device inputs -- the sm_100a hull vs the C restatement (oracle).
-    python tools/stress.py [cases] [seed]"""
+host and device inputs -- the sm_100a hull vs the compiled reference
+(oracle/_ref: seghull::hull::run, Sequential) or, with --port, the C restatement.
+Every 4th case also runs the multi-GPU entry point (sh_b200_hull_multi, 3 shards on
+one device) against the same expected hull.
+    python tools/stress.py [cases] [seed] [--port]"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
@@ -9,8 +12,12 @@ import torch
 import oracle
 from paper_1501_04706_b200 import dataio, hull
 
-cases = int(sys.argv[1]) if len(sys.argv) > 1 else 120
-rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
+argv = [a for a in sys.argv[1:] if not a.startswith("--")]
+cases = int(argv[0]) if len(argv) > 0 else 120
+rng = np.random.default_rng(int(argv[1]) if len(argv) > 1 else 2024)
+use_ref = "--port" not in sys.argv and oracle.ref_available()
+print("expected hulls from", "the compiled reference (oracle/_ref)" if use_ref else "the C restatement",
+      flush=True)
 
 
 def shape(kind, n):
@@ -45,6 +52,7 @@ def shape(kind, n):
 
 kinds = ["uniform", "disk", "circle", "gauss", "clusters", "lattice", "line", "annulus", "dups"]
 bad = 0
+multi = 0
 t0 = time.time()
 for i in range(cases):
     kind = kinds[i % len(kinds)]
@@ -55,7 +63,7 @@ for i in range(cases):
     dev = rng.random() < 0.5
     for mode in (1, 2):
         try:
-            ref = oracle.hull_run(x, y, mode)
+            ref = oracle.ref_hull_run(x, y, mode=mode, backend=1) if use_ref else oracle.hull_run(x, y, mode)
         except oracle.OracleError as e:
             ref = e
         ids = None
@@ -86,4 +94,13 @@ for i in range(cases):
         if not ok:
             bad += 1
             print(f"FAIL {kind} n={n} m{mode} ids={use_ids} dev={dev}: h {len(r)} vs {ref.h}", flush=True)
-print(f"{cases} cases x 2 modes: {bad} failures ({time.time() - t0:.0f} s)", flush=True)
+        if i % 4 == 0 and mode == 1 and not use_ids and n >= 3:
+            m = hull.run_multi(x, y, [0, 0, 0], mode)
+            okm = (len(m) == ref.h and np.array_equal(m.x.view(np.uint64), ref.x.view(np.uint64))
+                   and np.array_equal(m.indices, oracle.canonical_index(x, y, ref.x, ref.y)))
+            multi += 1
+            if not okm:
+                bad += 1
+                print(f"FAIL multi {kind} n={n}: h {len(m)} vs {ref.h}", flush=True)
+print(f"{cases} cases x 2 modes (+{multi} multi-GPU-entry checks): {bad} failures "
+      f"({time.time() - t0:.0f} s)", flush=True)
