@@ -264,3 +264,27 @@ def test_concurrent_pageable_callers():
     for t in th:
         t.join()
     assert not errors, errors
+
+
+def test_hull_multi_near_collinear_matches_reference_sharded_route():
+    """Nearly collinear input: the reference's own hull(union of shard hulls)
+    differs from its whole-input hull (FP predicates see different neighbours;
+    tests/test_oracle.py), so the multi-GPU entry is held to the reference's
+    sharded route (SURVEY 8d): 3 contiguous shards, hull::run of each, hull::run
+    of their union."""
+    torch_cuda()
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(5)
+    for n in (42, 7_428, 200_000):
+        t = rng.uniform(-1, 1, n)
+        x, y = t, 3 * t - 1 + (rng.random(n) < 0.001) * 1e-9
+        px, py = [], []
+        for g in range(3):
+            a, b = n * g // 3, n * (g + 1) // 3
+            r = oracle.ref_hull_run(x[a:b], y[a:b], mode=1)
+            px.append(r.x)
+            py.append(r.y)
+        sh = oracle.ref_hull_run(np.concatenate(px), np.concatenate(py), mode=1)
+        m = hull.run_multi(x, y, [0, 0, 0], 1)
+        same_hull(m, sh.x, sh.y, oracle.canonical_index(x, y, sh.x, sh.y), f"line {n}")

@@ -53,6 +53,7 @@ def shape(kind, n):
 kinds = ["uniform", "disk", "circle", "gauss", "clusters", "lattice", "line", "annulus", "dups"]
 bad = 0
 multi = 0
+multi_nonexact = 0
 t0 = time.time()
 for i in range(cases):
     kind = kinds[i % len(kinds)]
@@ -95,12 +96,36 @@ for i in range(cases):
             bad += 1
             print(f"FAIL {kind} n={n} m{mode} ids={use_ids} dev={dev}: h {len(r)} vs {ref.h}", flush=True)
         if i % 4 == 0 and mode == 1 and not use_ids and n >= 3:
+            # the multi-GPU entry (3 contiguous shards on this device) against the
+            # reference's own sharded route: hull::run of the union of the 3 shard
+            # hulls.  In general position that IS the whole-input hull;
+            # for near-collinear inputs the reference's sharded route itself differs
+            # from its whole-input hull (FP predicates), and the device must match
+            # the sharded route
             m = hull.run_multi(x, y, [0, 0, 0], mode)
-            okm = (len(m) == ref.h and np.array_equal(m.x.view(np.uint64), ref.x.view(np.uint64))
-                   and np.array_equal(m.indices, oracle.canonical_index(x, y, ref.x, ref.y)))
+            if use_ref:
+                parts = []
+                for g in range(3):
+                    a, b = n * g // 3, n * (g + 1) // 3
+                    if b > a:
+                        try:
+                            rr = oracle.ref_hull_run(x[a:b], y[a:b], mode=1, backend=0)
+                            parts.append((rr.x, rr.y))
+                        except oracle.OracleError:
+                            pass
+                sh = oracle.ref_hull_run(np.concatenate([p[0] for p in parts]),
+                                         np.concatenate([p[1] for p in parts]), mode=1, backend=0)
+            else:
+                sh = ref
+            okm = (len(m) == sh.h and np.array_equal(m.x.view(np.uint64), sh.x.view(np.uint64))
+                   and np.array_equal(m.y.view(np.uint64), sh.y.view(np.uint64))
+                   and np.array_equal(m.indices, oracle.canonical_index(x, y, sh.x, sh.y)))
             multi += 1
+            if not (sh.h == ref.h and np.array_equal(sh.x.view(np.uint64), ref.x.view(np.uint64))):
+                multi_nonexact += 1
             if not okm:
                 bad += 1
-                print(f"FAIL multi {kind} n={n}: h {len(m)} vs {ref.h}", flush=True)
-print(f"{cases} cases x 2 modes (+{multi} multi-GPU-entry checks): {bad} failures "
-      f"({time.time() - t0:.0f} s)", flush=True)
+                print(f"FAIL multi {kind} n={n}: h {len(m)} vs sharded reference {sh.h}", flush=True)
+print(f"{cases} cases x 2 modes (+{multi} multi-GPU-entry checks vs the reference's sharded route, "
+      f"{multi_nonexact} of them near-collinear inputs where that route differs from the whole-input "
+      f"hull): {bad} failures ({time.time() - t0:.0f} s)", flush=True)
