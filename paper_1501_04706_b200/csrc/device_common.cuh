@@ -14,6 +14,14 @@
 
 #define SH_DEV __device__ __forceinline__
 
+// Kernel-boundary probes (tools/prof_once.py with TRACE_ROUND=255): compiled
+// in only with -DSHB_PROBES, so the production kernels carry no extra code.
+#ifdef SHB_PROBES
+#define SHB_PROBE(...) __VA_ARGS__
+#else
+#define SHB_PROBE(...)
+#endif
+
 namespace shb {
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;

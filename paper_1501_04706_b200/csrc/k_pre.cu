@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(Cfg1::TPB, 1) k1_extremes(Bufs B) {
   // this CTA's extremes -> its partial (the next kernel combines them)
   K1Partial* part = B.k1part + blockIdx.x;
   cta_extremes(e, bad, part->e, &part->bad);
-  if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[1024 + blockIdx.x] = globaltimer_ns();
+  SHB_PROBE(if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[1024 + blockIdx.x] = globaltimer_ns());
 }
 
 // ===========================================================================
@@ -313,17 +313,17 @@ SH_DEV void combine_k1(const Bufs& B, Fin& s_fin, bool publish) {
   }
   __shared__ ExtRec s_ext[4];
   __shared__ unsigned long long s_bad;
-  const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u;
-  if (probe) B.dbg[1608] = globaltimer_ns() + (unsigned long long)(e[0].x == -1.0);
+  SHB_PROBE(const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u);
+  SHB_PROBE(if (probe) B.dbg[1608] = globaltimer_ns() + (unsigned long long)(e[0].x == -1.0));
   cta_extremes(e, bad, s_ext, &s_bad);
   __syncthreads();
-  if (probe) B.dbg[1609] = globaltimer_ns();
+  SHB_PROBE(if (probe) B.dbg[1609] = globaltimer_ns());
   if (threadIdx.x == 0) {
     const ExtRec ee[4] = {s_ext[0], s_ext[1], s_ext[2], s_ext[3]};
     compute_fin(s_fin, ee, s_bad);
     if (publish && blockIdx.x == 0) {
       write_fin(c, s_fin);
-      if (c->tl_round == 255u) B.dbg[1610] = globaltimer_ns();
+      SHB_PROBE(if (c->tl_round == 255u) B.dbg[1610] = globaltimer_ns());
       const unsigned long long now = globaltimer_ns() - c->t0_ns;
       c->mark[0] = now;
       c->mark[1] = now;
@@ -354,10 +354,10 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
   __syncthreads();
   // the points do not depend on K1: start the ring before waiting for it
   const uint32_t pre = stream_prefetch(R, B.n, B.in_x, B.in_y, B.in_id, SHB_K2_REVERSE != 0, true);
-  const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u;
-  if (probe) B.dbg[1600] = globaltimer_ns();
+  SHB_PROBE(const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u);
+  SHB_PROBE(if (probe) B.dbg[1600] = globaltimer_ns());
   pdl_wait();               // K1's partial extremes are complete and visible
-  if (probe) B.dbg[1601] = globaltimer_ns();
+  SHB_PROBE(if (probe) B.dbg[1601] = globaltimer_ns());
   pdl_launch_dependents();  // K3 may be scheduled on SMs this kernel frees
   // ---- every CTA combines K1's per-CTA extremes (no serial last-CTA step) ----
   __shared__ Fin s_fin;
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
       part->kept = s_kb;
       part->noncol = s_nc;
       if (blockIdx.x == 0) c->mark[2] = globaltimer_ns() - c->t0_ns;
-      if (c->tl_round == 255u) B.dbg[1200 + blockIdx.x] = globaltimer_ns();
+      SHB_PROBE(if (c->tl_round == 255u) B.dbg[1200 + blockIdx.x] = globaltimer_ns());
     }
   }
 }

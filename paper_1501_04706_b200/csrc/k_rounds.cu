@@ -236,7 +236,10 @@ struct K3Layout {
   static constexpr size_t kBytes = kRing;
 };
 
-template <bool IDS>
+// CAPPED: the live set is lean (runs shorter than a CTA's input share), so
+// every append is checked against the run (ST_OVERFLOW -> regrow, rerun); ~2%
+// of K3, paid only where the workspace is lean (n > 2^24)
+template <bool IDS, bool CAPPED>
 __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   using L = K3Layout<IDS>;
@@ -246,7 +249,6 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   __shared__ unsigned long long s_db[4];
   __shared__ SlotRec s_rec[4];
   __shared__ uint32_t s_off, s_Sn, s_Slon;
-  __shared__ uint32_t s_ws[MAXW + 1];
   __shared__ int s_last;
   Ctl* c = B.ctl;
   if (threadIdx.x == 0) R.init();
@@ -254,10 +256,10 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   // the points do not depend on K2 (their class bits do): start the ring on
   // them before waiting; the bits follow once K2 is complete
   const uint32_t pre = stream_prefetch(R, B.n, B.in_x, B.in_y, B.in_id, false, false);
-  const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u;
-  if (probe) B.dbg[1602] = globaltimer_ns();
+  SHB_PROBE(const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u);
+  SHB_PROBE(if (probe) B.dbg[1602] = globaltimer_ns());
   pdl_wait();               // K2's classes and partials are complete and visible
-  if (probe) B.dbg[1603] = globaltimer_ns();
+  SHB_PROBE(if (probe) B.dbg[1603] = globaltimer_ns());
   pdl_launch_dependents();  // the round kernel may be scheduled on SMs this kernel frees
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) {
     stream_drain_points(R, pre, B.n, reinterpret_cast<const unsigned char*>(B.bits));
@@ -302,9 +304,9 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
       s_kept = 0;
       s_nc = 0;
     }
-    if (probe) B.dbg[1606] = globaltimer_ns() + ((key[0][0] ^ kb) == 1ull ? 1ull : 0ull);
+    SHB_PROBE(if (probe) B.dbg[1606] = globaltimer_ns() + ((key[0][0] ^ kb) == 1ull ? 1ull : 0ull));
     cta_lexmin<2, 4>(key, valid, s_best2, win);  // starts with a barrier
-    if (probe) B.dbg[1607] = globaltimer_ns();
+    SHB_PROBE(if (probe) B.dbg[1607] = globaltimer_ns());
     {  // one shared atomic per warp (threads past the grid hold zeros)
       unsigned long long wk = kb;
 #pragma unroll
@@ -470,8 +472,11 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
                           (db >= *(volatile unsigned long long*)&s_db[pseg[q] & 3u])) << q;
     }
     if (__any_sync(FULL, candm)) contend_tile<K3_NP>(s_db, s_rec, candm, px, py, pd, pid, pseg, lowm);
-    run_append<K3_NP, true>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, run_base, pd, 0u, nullptr,
-                            nullptr, run_base + B.run_q, &c->status);
+    if (CAPPED)
+      run_append<K3_NP, true>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, run_base, pd, 0u, nullptr,
+                              nullptr, run_base + B.run_q, &c->status);
+    else
+      run_append<K3_NP>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, run_base);
   };
   stream_input(R, n, X, Y, I, reinterpret_cast<const unsigned char*>(B.bits), false,
                [&](int s, uint32_t first, uint32_t cnt) {
@@ -484,7 +489,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
 
   // ---- flush the CTA's records to the global slots of round 2's argmax ----
   __syncthreads();
-  if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[1400 + blockIdx.x] = globaltimer_ns();
+  SHB_PROBE(if (threadIdx.x == 0 && c->tl_round == 255u) B.dbg[1400 + blockIdx.x] = globaltimer_ns());
   if (threadIdx.x == 0 && (s_off & 1u) && s_off < B.run_q) {  // pad the run to an even length
     Oxy[run_base + s_off] = make_double2(0.0, 0.0);
     Ois[run_base + s_off] = make_uint2(NONE, NONE);
@@ -505,8 +510,8 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   // the last CTA combines the CTAs' rows: one thread per row, every field
   // loaded in one round trip, run counts summed per warp
   if (!s_last) return;
-  const bool probe_c = threadIdx.x == 0 && c->tl_round == 255u;
-  if (probe_c) B.dbg[1611] = globaltimer_ns();
+  SHB_PROBE(const bool probe_c = threadIdx.x == 0 && c->tl_round == 255u);
+  SHB_PROBE(if (probe_c) B.dbg[1611] = globaltimer_ns());
   __threadfence();
   __shared__ uint32_t s_mn;
   {  // the farthest record of each segment over the CTAs' rows -> Srec[1]
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
     }
     __syncthreads();
     if (lane == 0 && wsum) atomicAdd(&s_mn, wsum);
-    if (probe_c) B.dbg[1612] = globaltimer_ns();
+    SHB_PROBE(if (probe_c) B.dbg[1612] = globaltimer_ns());
     cta_lexmin<4, 4>(key, valid, s_best4, win);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -551,7 +556,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   }
   if (threadIdx.x != 0) return;
   const uint32_t mn = s_mn;
-  if (probe_c) B.dbg[1613] = globaltimer_ns();
+  SHB_PROBE(if (probe_c) B.dbg[1613] = globaltimer_ns());
   c->ticket = 0;
   const uint32_t before = c->S_cur + c->m_cur;
   StatRec st;
@@ -1171,10 +1176,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
   __shared__ uint32_t s_off, s_coff;
   __shared__ uint32_t s_pref[MAX_RUNS + 1];
   Ctl* c = B.ctl;
-  const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u;
-  if (probe) B.dbg[1604] = globaltimer_ns();
+  SHB_PROBE(const bool probe = blockIdx.x == 0 && threadIdx.x == 0 && c->tl_round == 255u);
+  SHB_PROBE(if (probe) B.dbg[1604] = globaltimer_ns());
   pdl_wait();  // round 1 (K3) is complete and visible
-  if (probe) B.dbg[1605] = globaltimer_ns();
+  SHB_PROBE(if (probe) B.dbg[1605] = globaltimer_ns());
   if (*(volatile uint32_t*)&c->status != ST_RUNNING) return;
   uint32_t r = *(volatile uint32_t*)&c->round + 1;
   const uint32_t trace_r = c->tl_round;  // debug timeline of CTA 0 in this round (0: off)
@@ -1595,11 +1600,18 @@ int rounds_blocks_per_sm() {
 }
 
 cudaError_t configure_stream_kernels_k3() {
-  cudaError_t e = cudaFuncSetAttribute(k3_round1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k3_round1<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)K3Layout<false>::kBytes);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k3_round1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)K3Layout<true>::kBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k3_round1<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)K3Layout<false>::kBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k3_round1<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)K3Layout<true>::kBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k3_round1<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)K3Layout<true>::kBytes);
+  return e;
 }
 
 template <class K>
@@ -1625,11 +1637,13 @@ static cudaError_t launch_pdl(K kernel, int grid, int block, size_t smem, cudaSt
   return cudaLaunchKernelEx(&cfg, kernel, B);
 }
 
-void launch_k3(const Bufs& B, bool ids, int grid, cudaStream_t s) {
+void launch_k3(const Bufs& B, bool ids, bool capped, int grid, cudaStream_t s) {
+  const size_t sm = ids ? K3Layout<true>::kBytes : K3Layout<false>::kBytes;
   if (ids)
-    launch_pdl(k3_round1<true>, grid, Cfg3::TPB, K3Layout<true>::kBytes, s, B, false);
+    launch_pdl(capped ? k3_round1<true, true> : k3_round1<true, false>, grid, Cfg3::TPB, sm, s, B, false);
   else
-    launch_pdl(k3_round1<false>, grid, Cfg3::TPB, K3Layout<false>::kBytes, s, B, false);
+    launch_pdl(capped ? k3_round1<false, true> : k3_round1<false, false>, grid, Cfg3::TPB, sm, s, B,
+               false);
 }
 
 cudaError_t launch_rounds(const Bufs& B, int grid, cudaStream_t s) {

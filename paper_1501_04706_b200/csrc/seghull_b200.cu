@@ -27,7 +27,7 @@ namespace shb {
 void launch_k1(const Bufs& B, bool ids, int grid, cudaStream_t s);
 void launch_small(const Bufs& B, bool filter, bool ids, cudaStream_t s);
 void launch_k2(const Bufs& B, bool filter, bool ids, int grid, cudaStream_t s);
-void launch_k3(const Bufs& B, bool ids, int grid, cudaStream_t s);
+void launch_k3(const Bufs& B, bool ids, bool capped, int grid, cudaStream_t s);
 cudaError_t configure_stream_kernels_pre();
 cudaError_t configure_stream_kernels_k3();
 size_t rounds_smem_bytes();
@@ -178,15 +178,19 @@ DeviceInfo device_info(int device) {
 }
 
 // Segment-table and live-set capacities of a fresh workspace.  Up to 2^24
-// points every point may become a head and every point may survive round 1.
-// Beyond, the tables start at n/16 segments (140 B each) and the live sets at
-// 3n/8 points (64 B each: two 24-B ping-pong sets + the 16-B contender list):
+// points every point may become a head, up to 2^27 every point may survive
+// round 1.  Beyond, the tables start at n/16 segments (140 B each) and the
+// live sets at 3n/8 points (64 B each: two 24-B ping-pong sets + the 16-B
+// contender list):
 // uniform 1B needs 55 heads and 0.23 n round-1 survivors.  An input that
 // outgrows either ends the call with ST_OVERFLOW; the call then regrows the
 // workspace to n + 2 segments and n live points and reruns (the grown
 // workspace stays in the pool for the next call).
 // SHB_SEG_CAP / SHB_LIVE_CAP (tests) cap them to force that path on small inputs.
-constexpr uint64_t LEAN_N = 1ull << 24;  // above this, tables and live sets start lean
+#ifndef SHB_LEAN_LOG2
+#define SHB_LEAN_LOG2 24
+#endif
+constexpr uint64_t LEAN_N = 1ull << SHB_LEAN_LOG2;  // above this, tables and live sets start lean
 
 uint64_t seg_capacity(uint64_t n) {
   uint64_t cap = n <= LEAN_N ? n + 2 : std::max<uint64_t>(LEAN_N, n / 16);
@@ -197,8 +201,11 @@ uint64_t seg_capacity(uint64_t n) {
   return cap;
 }
 
+constexpr uint64_t LEAN_LIVE_N = 1ull << 27;  // live sets start lean above this
+
 uint64_t live_capacity(uint64_t n) {
-  uint64_t cap = n <= LEAN_N ? n : std::max<uint64_t>(LEAN_N, (3 * n / 8 + 63) & ~63ull);
+  // full up to 2^27 points (8.6 GB): K3 then needs no per-append check
+  uint64_t cap = n <= LEAN_LIVE_N ? n : std::max<uint64_t>(LEAN_N, (3 * n / 8 + 63) & ~63ull);
   if (const char* e = std::getenv("SHB_LIVE_CAP")) {  // tests: force K3's overflow check
     const uint64_t v = std::strtoull(e, nullptr, 10);
     if (v >= 4096) cap = std::min(cap, v);
@@ -554,13 +561,14 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   const uint64_t ntiles3 = (n + Cfg3::T - 1) / Cfg3::T;
   // a run holds the CTA's whole input share, or (lean live sets) an even
   // 1/gs of the live capacity -- K3 then checks every append against it
-  B.run_q = (uint32_t)std::min<uint64_t>((ntiles3 + gs - 1) / gs * Cfg3::T,
-                                         (ws.live_n / gs) & ~1ull);
+  const uint64_t share = (ntiles3 + gs - 1) / gs * Cfg3::T;  // a K3 CTA's input share
+  B.run_q = (uint32_t)std::min<uint64_t>(share, (ws.live_n / gs) & ~1ull);
+  const bool capped = B.run_q < share;  // lean live set: K3 checks its appends
   // K1 -> K2 -> K3 -> rounds with programmatic dependent launch: no events
   // between them (per-kernel times come from device %globaltimer marks)
   launch_k1(B, ids, g1, st);
   launch_k2(B, rq.mode == SH_MODE_WITH_PREPROCESS, ids, g2, st);
-  launch_k3(B, ids, gs, st);
+  launch_k3(B, ids, capped, gs, st);
   CK(cudaGetLastError());
   // the round kernel's CTA j owns run j of each live set: at most gs runs
   CK(launch_rounds(B, std::min(ws.rounds_grid, gs), st));
