@@ -498,8 +498,27 @@ void d2h_ring(Workspace& ws, void* dst, const void* src, size_t n, bool widen, u
 // Runs the whole pipeline with ONE host synchronisation: H2D (host inputs),
 // K1, K2, K3, the cooperative round kernel, K5 (device outputs), and the
 // read-back of the control block + the first STATS_EAGER round stats.
+// SHB_HOST_TIMING=1: host-side wall clock of one call's steps on stderr (debug)
+const bool g_host_timing = std::getenv("SHB_HOST_TIMING") != nullptr;
+struct HostClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  char buf[512];
+  int len = 0;
+  void mark(const char* what) {
+    if (!g_host_timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    len += std::snprintf(buf + len, sizeof(buf) - len, " %s %.1f",
+                         what, std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+  }
+  void print() {
+    if (g_host_timing) std::fprintf(stderr, "[host us]%s\n", buf);
+  }
+};
+
 RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& res,
                     cudaStream_t st, bool timings, const uint32_t* n_dev = nullptr) {
+  HostClock hc;
   RunOut out;
   Bufs B = ws.B;
   const uint64_t n = rq.n;
@@ -532,8 +551,10 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   B.n_dev = n <= SMALL_N ? n_dev : nullptr;
   const bool ids = B.in_id != nullptr;
 
+  hc.mark("stage");
   // a zeroed control block is the initial state (ST_RUNNING == 0)
   CK(cudaMemsetAsync(B.ctl, 0, sizeof(Ctl), st));
+  hc.mark("memset");
   if (g_trace_round) {
     const uint32_t tr = (uint32_t)g_trace_round;
     CK(cudaMemcpyAsync(&B.ctl->tl_round, &tr, sizeof(tr), cudaMemcpyHostToDevice, st));
@@ -574,6 +595,7 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   CK(launch_rounds(B, std::min(ws.rounds_grid, gs), st));
   out.launches = 4;
   }
+  hc.mark("launch");
   if (timings) CK(cudaEventRecord(ws.ev[5], st));
   const bool out_dev = (rq.flags & SH_OUT_DEVICE) != 0;
   if (out_dev && (rq.flags & SH_OUT_PAD)) {
@@ -589,7 +611,10 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   CK(cudaMemcpyAsync(ws.h_res, B.ctl, HOST_RES_BYTES, cudaMemcpyDeviceToHost, st));
   const bool want_stats = res.stats && res.stats_cap && !(rq.flags & SH_NO_STATS);
   if (timings) CK(cudaEventRecord(ws.ev[6], st));
+  hc.mark("k5+d2h");
   CK(cudaStreamSynchronize(st));
+  hc.mark("sync");
+  hc.print();
   if (want_stats)
     std::memcpy(ws.h_stats, ws.h_res + HOST_RES_STATS,
                 sizeof(StatRec) * std::min<uint64_t>(ws.h_ctl->round, STATS_EAGER));

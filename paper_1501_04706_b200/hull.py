@@ -566,17 +566,19 @@ def pack_device(x, y, block, *, first: int = 0, mode: int = Mode.WithPreprocess,
 
 
 def hull_gathered(payload, nblocks: int, n_total: int, mode: int = Mode.WithPreprocess, *,
-                  stream: int | None = None, out_device: bool = True):
+                  stream: int | None = None, out_device: bool = True, out=None):
     """The merge step of a one-process-per-GPU run: ``payload`` is the
     all-gathered float64 CUDA tensor of ``nblocks`` pack_device blocks.
-    Returns (x, y, indices) -- device tensors when out_device -- or raises
-    Error / returns None when a block overflowed: then (None, needed_cap)."""
+    Returns ((x, y, indices), h) -- device tensors when out_device, written
+    into ``out`` = (x, y, idx) buffers of nblocks * block_cap entries when
+    given -- or (None, needed_cap) when a block overflowed."""
     import torch
     L = _lib.load()
     device = int(payload.device.index)
     bcap = int(payload.numel()) // (3 * nblocks)
     cap = max(2, nblocks * bcap)
-    bufs = _multi_out(cap, out_device, device)
+    bufs = out if out is not None else _multi_out(cap, out_device, device)
+    cap = min(cap, int(bufs[0].shape[0]))
     if stream is None:
         stream = torch.cuda.current_stream(payload.device).cuda_stream
     h = ctypes.c_uint64(0)

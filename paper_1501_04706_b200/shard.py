@@ -65,13 +65,27 @@ def merged_hull(x, y, first: int, n_total: int, world: int,
         raise ValueError("global indices exceed the 32-bit ids of the C-ABI")
     cap = block_cap
     while True:
-        block = torch.empty(3 * cap, dtype=torch.float64, device=dev)
+        # the block, the gathered payload and the merge outputs are reused
+        # from step to step (a repeated step allocates nothing)
+        key = (str(dev), cap, world, bool(out_device))
+        bufs = _BUFS.get(key)
+        if bufs is None:
+            mo = None
+            if out_device and dev.type == "cuda":
+                mo = tuple(torch.empty(world * cap, dtype=dt, device=dev)
+                           for dt in (torch.float64, torch.float64, torch.int64))
+            bufs = _BUFS[key] = (torch.empty(3 * cap, dtype=torch.float64, device=dev),
+                                 torch.empty(world * 3 * cap, dtype=torch.float64, device=dev), mo)
+        block, gathered, mo = bufs
         pack(x, y, block, first=first, mode=mode, stream=stream)
-        gathered = torch.empty(world * 3 * cap, dtype=torch.float64, device=dev)
         all_gather_into_tensor(gathered, block)
-        res, k = merge(gathered, world, n_total, mode, stream=stream, out_device=out_device)
+        kw = {"out": mo} if mo is not None else {}
+        res, k = merge(gathered, world, n_total, mode, stream=stream, out_device=out_device, **kw)
         if res is not None:
             return res, k
         if k <= cap:
             raise RuntimeError(f"merge reported capacity {k} <= block capacity {cap}")
         cap = k  # some shard hull outgrew the block: every rank retries with its size
+
+
+_BUFS: dict = {}
