@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SH_B200_ABI_VERSION 3
+#define SH_B200_ABI_VERSION 4
 
 /* return codes: 0 or 1 + seghull::Errc (error.hpp:8-19) */
 enum sh_status {
@@ -63,11 +63,17 @@ enum sh_flags {
   SH_NO_STATS = 4u,       /* skip the per-round stats read-back                    */
   SH_OUT_DEVICE = 8u,     /* out_idx/out_x/out_y are device memory on `device`:      */
                           /* the vertices never leave HBM (shard hulls -> gather)    */
-  SH_OUT_PAD = 16u        /* with SH_OUT_DEVICE: write ONE fixed-size payload block  */
+  SH_OUT_PAD = 16u,       /* with SH_OUT_DEVICE: write ONE fixed-size payload block  */
                           /* at out_x: {x f64[cap] | y f64[cap] | index i64[cap]},   */
                           /* the h vertices, then padding (copies of vertex 0 with   */
                           /* index -1); h > cap writes NaN x and h into index[0]     */
                           /* (see sh_b200_hull_gathered)                             */
+  SH_ASYNC = 32u          /* with SH_DEVICE_PTRS: sh_b200_hull_ex only enqueues the  */
+                          /* call on its stream and returns a ticket in res->ticket; */
+                          /* sh_b200_hull_wait(ticket, res) completes it.  The call  */
+                          /* keeps its workspace until then, so a caller can issue   */
+                          /* hull i+1 while hull i runs (host work off the GPU's     */
+                          /* critical path)                                          */
 };
 
 /* hull.hpp:35-40 SegmentStats, plus the device time at which the round ended */
@@ -146,9 +152,15 @@ typedef struct {
   sh_kernel_ms kernels;
   uint32_t kernel_launches; /* kernels this call launched (evidence of GPU work) */
   char err[256];
+  uint64_t ticket;      /* SH_ASYNC: the handle for sh_b200_hull_wait              */
 } sh_hull_result;
 
 int sh_b200_hull_ex(const sh_hull_request* req, sh_hull_result* res);
+
+/* Completes an SH_ASYNC call: waits for its device work, then fills `res` like
+ * a synchronous call (outputs in the buffers given at submission; `res->stats`
+ * may name a stats buffer now).  Each ticket is waited for exactly once. */
+int sh_b200_hull_wait(uint64_t ticket, sh_hull_result* res);
 
 /*
  * Multi-GPU hull (SURVEY.md section 8b "sh_b200_hull_multi", 8e; hull.hpp:95

@@ -45,7 +45,7 @@ class sh_hull_result(ctypes.Structure):
                 ("stats", _vp), ("stats_cap", _u64), ("rounds", _u64), ("kept", _u64),
                 ("bad_index", _u64), ("phases", sh_phase_ms), ("kernels", sh_kernel_ms),
                 ("kernel_launches", _u32),
-                ("err", ctypes.c_char * 256)]
+                ("err", ctypes.c_char * 256), ("ticket", _u64)]
 
 
 class sh_shard(ctypes.Structure):
@@ -75,7 +75,7 @@ EXPORTS = ("sh_b200_hull", "sh_b200_hull_ex", "sh_b200_gen_uniform", "sh_b200_ge
            "sh_b200_preprocess", "sh_b200_hull_multi", "sh_b200_hull_shards",
            "sh_b200_hull_gathered", "sh_b200_first_split", "sh_b200_compute_distances",
            "sh_b200_find_farthest", "sh_b200_split_segments", "sh_b200_mark_interior",
-           "sh_b200_compact")
+           "sh_b200_compact", "sh_b200_hull_wait")
 
 SH_HOST_PTRS = 0
 SH_DEVICE_PTRS = 1
@@ -83,7 +83,8 @@ SH_PHASE_TIMINGS = 2
 SH_NO_STATS = 4
 SH_OUT_DEVICE = 8
 SH_OUT_PAD = 16
-ABI_VERSION = 3
+SH_ASYNC = 32
+ABI_VERSION = 4
 
 _lib = None
 
@@ -101,6 +102,7 @@ def load() -> ctypes.CDLL:
     L.sh_b200_hull.argtypes = [_vp, _vp, _u64, ctypes.c_int, _u32, ctypes.c_int, _vp, _vp, _vp,
                                _u64, _vp, _vp, _u64, _vp, _vp, ctypes.c_char_p, ctypes.c_size_t]
     L.sh_b200_hull_ex.argtypes = [ctypes.POINTER(sh_hull_request), ctypes.POINTER(sh_hull_result)]
+    L.sh_b200_hull_wait.argtypes = [_u64, ctypes.POINTER(sh_hull_result)]
     L.sh_b200_gen_uniform.argtypes = [_vp, _vp, _u64, _u64, _u64, ctypes.c_int, _vp]
     L.sh_b200_gen_disk.argtypes = [_vp, _vp, _u64, _u64, ctypes.c_int, _vp]
     L.sh_b200_gen_circle_host.argtypes = [_vp, _vp, _u64, _u64]

@@ -18,6 +18,7 @@
 #include <chrono>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/seghull_b200.h"
@@ -516,8 +517,14 @@ struct HostClock {
   }
 };
 
+RunOut parse_ctl(Workspace& ws, const sh_hull_request& rq, const sh_hull_result& res);
+
+// Enqueues the whole pipeline; with `wait` it synchronises and parses the
+// control block, otherwise it returns code -2 (pending): ws.ev[7] marks the
+// end of the call's device work, parse_ctl() finishes it later.
 RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& res,
-                    cudaStream_t st, bool timings, const uint32_t* n_dev = nullptr) {
+                    cudaStream_t st, bool timings, const uint32_t* n_dev = nullptr,
+                    bool wait = true) {
   HostClock hc;
   RunOut out;
   Bufs B = ws.B;
@@ -612,9 +619,26 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   const bool want_stats = res.stats && res.stats_cap && !(rq.flags & SH_NO_STATS);
   if (timings) CK(cudaEventRecord(ws.ev[6], st));
   hc.mark("k5+d2h");
+  if (!wait) {
+    CK(cudaEventRecord(ws.ev[7], st));
+    out.code = -2;
+    return out;
+  }
   CK(cudaStreamSynchronize(st));
   hc.mark("sync");
   hc.print();
+  (void)want_stats;
+  RunOut parsed = parse_ctl(ws, rq, res);
+  parsed.launches = out.launches;
+  return parsed;
+}
+
+// The control block of a finished call (in ws.h_res) -> RunOut.
+RunOut parse_ctl(Workspace& ws, const sh_hull_request& rq, const sh_hull_result& res) {
+  RunOut out;
+  const uint64_t n = rq.n;
+  const Bufs& B = ws.B;
+  const bool want_stats = res.stats && res.stats_cap && !(rq.flags & SH_NO_STATS);
   if (want_stats)
     std::memcpy(ws.h_stats, ws.h_res + HOST_RES_STATS,
                 sizeof(StatRec) * std::min<uint64_t>(ws.h_ctl->round, STATS_EAGER));
@@ -665,6 +689,22 @@ RunOut run_pipeline(Workspace& ws, const sh_hull_request& rq, sh_hull_result& re
   return out;
 }
 
+int hull_finish(std::unique_ptr<Workspace>& ws, const sh_hull_request& rqv, sh_hull_result* res,
+                cudaStream_t st, bool timings, RunOut o, std::unique_ptr<Workspace>* keep,
+                const uint32_t* n_dev, int prev_dev);
+
+// An SH_ASYNC call between sh_b200_hull_ex and sh_b200_hull_wait: its request,
+// output description, stream and the workspace it holds.
+struct Pending {
+  sh_hull_request rq;
+  sh_hull_result res;
+  cudaStream_t st = nullptr;
+  uint32_t launches = 0;
+  std::unique_ptr<Workspace> ws;
+};
+std::unordered_map<uint64_t, std::unique_ptr<Pending>> g_pending;  // under g_mutex
+uint64_t g_ticket = 0;
+
 // One hull on one device.  `keep`: on success the workspace is handed back to
 // the caller instead of the pool (the multi-GPU path re-packs from its final
 // head table when a shard hull outgrew the payload).
@@ -703,7 +743,48 @@ int hull_impl(const sh_hull_request* rq, sh_hull_result* res,
     ws = acquire(rq->device, n);
     const bool timings = (rq->flags & SH_PHASE_TIMINGS) != 0;
     cudaStream_t st = rq->stream ? (cudaStream_t)rq->stream : ws->stream;
+    if (rq->flags & SH_ASYNC) {  // enqueue only; sh_b200_hull_wait finishes
+      RunOut o = run_pipeline(*ws, *rq, *res, st, timings, n_dev, false);
+      auto pd = std::make_unique<Pending>();
+      pd->launches = o.launches;
+      pd->rq = *rq;
+      pd->res = *res;
+      pd->st = st;
+      pd->ws = std::move(ws);
+      {
+        std::lock_guard<std::mutex> lk(g_mutex);
+        res->ticket = ++g_ticket;
+        g_pending[res->ticket] = std::move(pd);
+      }
+      cudaSetDevice(prev_dev);
+      return SH_OK;
+    }
     RunOut o = run_pipeline(*ws, *rq, *res, st, timings, n_dev);
+    return hull_finish(ws, *rq, res, st, timings, o, keep, n_dev, prev_dev);
+  } catch (const CudaFail& f) {
+    put_err(res->err, sizeof(res->err),
+            std::string("CUDA error: ") + cudaGetErrorString(f.err) + " at " + f.what);
+    cudaGetLastError();
+    ws.reset();  // a failed workspace is not returned to the pool
+    cudaSetDevice(prev_dev);
+    return SH_CUDA_ERROR;
+  } catch (const std::bad_alloc&) {
+    put_err(res->err, sizeof(res->err), "host allocation failed");
+    cudaSetDevice(prev_dev);
+    return SH_CUDA_ERROR;
+  }
+}
+
+// Everything after the pipeline ran: overflow regrow + rerun, outputs, stats,
+// timings, workspace back to the pool (or to *keep).
+int hull_finish(std::unique_ptr<Workspace>& ws, const sh_hull_request& rqv, sh_hull_result* res,
+                cudaStream_t st, bool timings, RunOut o, std::unique_ptr<Workspace>* keep,
+                const uint32_t* n_dev, int prev_dev) {
+  const sh_hull_request* rq = &rqv;
+  const uint64_t n = rq->n;
+  const bool out_dev = (rq->flags & SH_OUT_DEVICE) != 0;
+  const bool pad = (rq->flags & SH_OUT_PAD) != 0;
+  try {
     if (o.code == -1) {  // segment tables or live sets too small: regrow to the worst case, rerun
       const int dev = ws->device;
       const uint64_t cap = std::max<uint64_t>(n, 1u << 12);
@@ -1158,7 +1239,47 @@ int sh_b200_debug_last_timeline(unsigned long long* out, int cap) {
   return n;
 }
 
-int sh_b200_hull_ex(const sh_hull_request* req, sh_hull_result* res) { return hull_impl(req, res); }
+int sh_b200_hull_ex(const sh_hull_request* req, sh_hull_result* res) {
+  if (req && (req->flags & SH_ASYNC) && !(req->flags & SH_DEVICE_PTRS)) return SH_INVALID_ARGUMENT;
+  if (res) res->ticket = 0;
+  return hull_impl(req, res);
+}
+
+int sh_b200_hull_wait(uint64_t ticket, sh_hull_result* res) {
+  if (!res) return SH_INVALID_ARGUMENT;
+  std::unique_ptr<Pending> pd;
+  {
+    std::lock_guard<std::mutex> lk(g_mutex);
+    auto it = g_pending.find(ticket);
+    if (it == g_pending.end()) return SH_INVALID_ARGUMENT;
+    pd = std::move(it->second);
+    g_pending.erase(it);
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  // the caller's stats buffer may be given here (the ticket keeps its outputs)
+  sh_hull_result r = pd->res;
+  r.stats = res->stats ? res->stats : r.stats;
+  r.stats_cap = res->stats ? res->stats_cap : r.stats_cap;
+  r.err[0] = 0;
+  try {
+    CK(cudaSetDevice(pd->rq.device));
+    CK(cudaEventSynchronize(pd->ws->ev[7]));
+    const bool timings = (pd->rq.flags & SH_PHASE_TIMINGS) != 0;
+    RunOut o = parse_ctl(*pd->ws, pd->rq, r);
+    o.launches = pd->launches;
+    const int rc = hull_finish(pd->ws, pd->rq, &r, pd->st, timings, o, nullptr, nullptr, prev);
+    r.ticket = ticket;
+    *res = r;
+    return rc;
+  } catch (const CudaFail& f) {
+    put_err(res->err, sizeof(res->err),
+            std::string("CUDA error: ") + cudaGetErrorString(f.err) + " at " + f.what);
+    cudaGetLastError();
+    cudaSetDevice(prev);
+    return SH_CUDA_ERROR;
+  }
+}
 
 int sh_b200_hull_shards(const sh_shard* shards, int nshards, int mode, uint32_t flags,
                         int root_device, int64_t* out_idx, double* out_x, double* out_y,

@@ -385,10 +385,13 @@ class DeviceHull:
 
 
 def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int | None = None,
-               timings: bool = False, stats: bool = True, out=None) -> DeviceHull:
+               timings: bool = False, stats: bool = True, out=None, wait: bool = True):
     """Hull of device-resident float64 CUDA tensors; the vertices are written to
     device tensors (``out`` = (x, y, idx) buffers of equal capacity, else
-    allocated at len(x)).  Only h, the stats and timings cross to the host."""
+    allocated at len(x)).  Only h, the stats and timings cross to the host.
+    ``wait=False`` (SH_ASYNC) only enqueues the call on the stream and returns a
+    :class:`PendingHull`; its ``result()`` completes it.  The host work of the
+    next call then overlaps this call's device work."""
     import torch
     x, y, ids, px, py, dx, n = _prepare(x, y, ids)
     if not dx:
@@ -403,12 +406,66 @@ def run_device(x, y, mode: int = Mode.WithPreprocess, *, ids=None, stream: int |
     if stream is None:
         stream = torch.cuda.current_stream(x.device).cuda_stream
     flags = _lib.SH_DEVICE_PTRS | _lib.SH_OUT_DEVICE | (_lib.SH_PHASE_TIMINGS if timings else 0)
+    if not wait:
+        return PendingHull(px, py, n, ids, mode, flags | _lib.SH_ASYNC
+                           | (0 if stats else _lib.SH_NO_STATS), device, stream, out,
+                           (1 << 16) if stats else 0, (x, y))
     res, sts, ph, kt, ends = _call(px, py, n, ids.data_ptr() if ids is not None else None, mode, flags,
                              device, stream, ox.data_ptr(), oy.data_ptr(), oi.data_ptr(),
                              int(ox.shape[0]), (1 << 16) if stats else 0)
     h = int(res.h)
     return DeviceHull(ox, oy, oi, h, sts, ph, kt, int(res.kept), int(res.rounds),
                       int(res.kernel_launches), ends[0], ends[1])
+
+
+class PendingHull:
+    """An SH_ASYNC hull (run_device(..., wait=False)): enqueued on its stream,
+    completed by result().  Keeps its inputs and outputs alive until then."""
+
+    def __init__(self, px, py, n, ids, mode, flags, device, stream, out, stats_cap, keep):
+        L = _lib.load()
+        self._req, self._res = _lib.sh_hull_request(), _lib.sh_hull_result()
+        req, res = self._req, self._res
+        req.x, req.y, req.n = px, py, n
+        req.ids = ids.data_ptr() if ids is not None else None
+        req.mode, req.flags, req.device = int(mode), flags, int(device)
+        req.stream = _lib.stream_handle(stream)
+        ox, oy, oi = out
+        res.x, res.y, res.idx, res.cap = ox.data_ptr(), oy.data_ptr(), oi.data_ptr(), int(ox.shape[0])
+        self._stats_cap = stats_cap
+        self._out, self._keep, self._done = out, keep, None
+        self._flags = flags
+        rc = L.sh_b200_hull_ex(ctypes.byref(req), ctypes.byref(res))
+        if rc != 0:
+            _raise(rc, res.err.decode(errors="replace"))
+
+    def result(self) -> "DeviceHull":
+        if self._done is not None:
+            return self._done
+        L = _lib.load()
+        res = self._res
+        st = (_lib.sh_round_stat * max(self._stats_cap, 1))() if self._stats_cap else None
+        res.stats = ctypes.addressof(st) if st is not None else None
+        res.stats_cap = self._stats_cap
+        rc = L.sh_b200_hull_wait(res.ticket, ctypes.byref(res))
+        if rc != 0:
+            _raise(rc, res.err.decode(errors="replace"))
+        nst = min(int(res.rounds), self._stats_cap)
+        raw = ctypes.string_at(ctypes.addressof(st), nst * _ROW) if nst else b""
+        if self._flags & _lib.SH_PHASE_TIMINGS:
+            ph = PhaseTimings(res.phases.pre_ms, res.phases.split_ms, res.phases.recurse_ms,
+                              res.phases.total_ms)
+            k = res.kernels
+            kt = KernelTimings(k.h2d_ms, k.extremes_ms, k.filter_ms, k.first_round_ms,
+                               k.rounds_ms, k.d2h_ms)
+        else:
+            ph, kt = _ZERO_PH, _ZERO_KT
+        ox, oy, oi = self._out
+        self._done = DeviceHull(ox, oy, oi, int(res.h), RoundList(raw, 0), ph, kt, int(res.kept),
+                                int(res.rounds), int(res.kernel_launches), RoundList(raw, 1),
+                                RoundList(raw, 2))
+        self._keep = None
+        return self._done
 
 
 def preprocess_device(x, y, *, stream: int | None = None):

@@ -33,7 +33,7 @@ def test_library_loads_and_exports_header_symbols():
     for s in syms:
         assert hasattr(L, s), f"{s} declared in include/ but not exported"
     assert set(_lib.EXPORTS) == syms
-    assert L.sh_b200_abi_version() == _lib.ABI_VERSION == 3
+    assert L.sh_b200_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_library_is_sm100a_cubin():

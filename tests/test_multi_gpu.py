@@ -15,6 +15,7 @@ regrow path and concurrent callers.
   stream, the default for host inputs).
 * two host threads with pageable inputs at once (per-workspace pinned rings).
 """
+import ctypes
 import os
 import threading
 
@@ -288,3 +289,37 @@ def test_hull_multi_near_collinear_matches_reference_sharded_route():
         sh = oracle.ref_hull_run(np.concatenate(px), np.concatenate(py), mode=1)
         m = hull.run_multi(x, y, [0, 0, 0], 1)
         same_hull(m, sh.x, sh.y, oracle.canonical_index(x, y, sh.x, sh.y), f"line {n}")
+
+
+def test_async_submission_matches_sync():
+    """SH_ASYNC: several hulls in flight on one stream (each holding its own
+    workspace), completed out of order, equal the synchronous results; a
+    ticket is waited for once; the overflow regrow also runs on completion."""
+    torch = torch_cuda()
+    L = _lib.load()
+    inputs_ = [dataio.gen_uniform_device(3_000_000, s) for s in (1, 2, 3)]
+    circle = dataio.gen_circle(200_000, 3)
+    inputs_.append((torch.from_numpy(circle[0]).cuda(), torch.from_numpy(circle[1]).cuda()))
+    sync = [hull.run_device(x, y, 1) for x, y in inputs_]
+    pend = [hull.run_device(x, y, 1, wait=False) for x, y in inputs_]
+    for i in (2, 0, 3, 1):
+        r = pend[i].result()
+        assert r.h == sync[i].h and r.rounds == sync[i].rounds
+        assert torch.equal(r.x, sync[i].x) and torch.equal(r.indices, sync[i].indices)
+        assert [tuple(vars(s).values()) for s in r.stats] == [tuple(vars(s).values()) for s in sync[i].stats]
+    res = _lib.sh_hull_result()
+    assert L.sh_b200_hull_wait(pend[0]._res.ticket, ctypes.byref(res)) == 102  # already waited
+    # host inputs cannot be asynchronous
+    with pytest.raises(RuntimeError):
+        hull.PendingHull(circle[0].ctypes.data, circle[1].ctypes.data, circle[0].size, None, 1,
+                         _lib.SH_ASYNC | _lib.SH_OUT_DEVICE, 0, None, hull._multi_out(8, True, 0), 0, None)
+    # the regrow-and-rerun path on completion
+    L.sh_b200_release_pool()
+    os.environ["SHB_SEG_CAP"] = "5000"
+    try:
+        r = hull.run_device(inputs_[3][0], inputs_[3][1], 1, wait=False).result()
+    finally:
+        del os.environ["SHB_SEG_CAP"]
+        L.sh_b200_release_pool()
+    assert r.h == sync[3].h and torch.equal(r.x, sync[3].x)
+    assert r.kernel_launches > 0
