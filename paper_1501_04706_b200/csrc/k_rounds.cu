@@ -90,7 +90,7 @@ SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py
                        const uint32_t (&pid)[NP], const uint32_t (&pseg)[NP], uint32_t* s_off,
                        double2* Oxy, uint2* Ois, uint32_t base, const double (&pd)[NP] = {},
                        uint32_t candm = 0, uint32_t* s_coff = nullptr, LiveCand* Oc = nullptr,
-                       uint32_t lim = 0, uint32_t* ovf = nullptr) {
+                       uint32_t lim = 0, uint32_t* ovf = nullptr, uint32_t* eo = nullptr) {
   const int lane = threadIdx.x & 31;
   uint32_t bal[NP];
   uint32_t tot = 0;
@@ -112,6 +112,7 @@ SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
     e[j] = off + __popc(bal[j] & lt);
+    if (eo != nullptr) eo[j] = e[j];
     if ((keepm >> j) & 1u) {
       Oxy[e[j]] = make_double2(px[j], py[j]);
       Ois[e[j]] = make_uint2(pid[j], pseg[j]);
@@ -139,6 +140,41 @@ SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py
       }
       co += __popc(cb[j]);
     }
+  }
+}
+
+// Contender list of a large-table tile whose atomicMax results arrived: the
+// survivors that reached the running maximum (db >= old) are listed
+// (distance, live position, segment) at Oc[base + ...] through s_coff.
+template <int NP>
+SH_DEV void list_cands(uint32_t m, const unsigned long long (&db)[NP],
+                       const unsigned long long (&old)[NP], const uint32_t (&pos)[NP],
+                       const uint32_t (&seg)[NP], uint32_t* s_coff, LiveCand* Oc, uint32_t base) {
+  uint32_t candm = 0;
+#pragma unroll
+  for (int j = 0; j < NP; ++j)
+    if (((m >> j) & 1u) && db[j] >= old[j]) candm |= 1u << j;
+  if (!__any_sync(FULL, candm)) return;
+  const uint32_t lane = threadIdx.x & 31, lt = lanemask_lt();
+  uint32_t cb[NP], ctot = 0;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    cb[j] = __ballot_sync(FULL, (candm >> j) & 1u);
+    ctot += __popc(cb[j]);
+  }
+  uint32_t co = 0;
+  if (lane == 0) co = atomicAdd(s_coff, ctot);
+  co = base + __shfl_sync(FULL, co, 0);
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    if ((candm >> j) & 1u) {
+      LiveCand lc;
+      lc.d = __longlong_as_double((long long)db[j]);
+      lc.pos = pos[j];
+      lc.seg = seg[j];
+      Oc[co + __popc(cb[j] & lt)] = lc;
+    }
+    co += __popc(cb[j]);
   }
 }
 
@@ -585,6 +621,9 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
 constexpr int RW = RTPB / 32;          // warps per CTA
 constexpr int KR_U = LIVE_T / RCTHREADS;  // live points per consumer thread per tile
 
+#ifndef SHB_DEFER
+#define SHB_DEFER 1  // large tables: consume a tile's atomicMax results one tile later
+#endif
 #ifndef SHB_MED
 #define SHB_MED 1
 #endif
@@ -1341,6 +1380,10 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
         }
       }
     } else {
+#if SHB_DEFER
+      unsigned long long q_db[KR_U], q_old[KR_U];  // the pending tile (large tables)
+      uint32_t q_pos[KR_U], q_seg[KR_U], q_m = 0;
+#endif
       for (uint32_t k = 0; k < ntl; ++k) {
         const int st = (int)((kbase + k) % LIVE_NS);
         const uint32_t ph = ((kbase + k) / LIVE_NS) & 1u;
@@ -1409,13 +1452,21 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
             if (lower) lowm |= 1u << u;
           }
         }
+#if !SHB_DEFER
         uint32_t candm = 0;
+#endif
         if (small) {
           contend_tile<KR_U>(sm.db, sm.rec, keepm, px, py, pd, pid, pseg, lowm);
         } else {
           // large table: max of the distance bits in the global slot; a
           // survivor that reached the running maximum is listed for the
           // winner pass after the barrier
+#if SHB_DEFER
+          // the previous tile's atomicMax results are consumed only now, so
+          // their L2 round trip overlapped this tile's route-row loads
+          list_cands<KR_U>(q_m, q_db, q_old, q_pos, q_seg, &s_coff, B.Lc, obase);
+          q_m = 0;
+#endif
 #pragma unroll
           for (int u = 0; u < KR_U; ++u) {
             if ((keepm >> u) & 1u) {
@@ -1424,13 +1475,28 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
               // below this CTA's running maximum: below the final one too
               if (med && db < atomicMax(mdb + pseg[u], db)) continue;
 #endif
+#if SHB_DEFER
+              q_db[u] = db;
+              q_seg[u] = pseg[u];
+              q_old[u] = atomicMax(Sd + pseg[u], db);
+              q_m |= 1u << u;
+#else
               if (db >= atomicMax(Sd + pseg[u], db)) candm |= 1u << u;
+#endif
             }
           }
         }
+#if SHB_DEFER
+        run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase, pd, 0u, nullptr,
+                         nullptr, 0u, nullptr, q_pos);
+#else
         run_append<KR_U>(keepm, px, py, pid, pseg, &s_off, Oxy, Ois, obase, pd, candm, &s_coff,
                          small ? nullptr : B.Lc);
+#endif
       }
+#if SHB_DEFER
+      if (!small) list_cands<KR_U>(q_m, q_db, q_old, q_pos, q_seg, &s_coff, B.Lc, obase);
+#endif
     }
     __syncthreads();
     KR_MARK();  // point loop done
