@@ -464,18 +464,21 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
       // d > 0 tests ignore) without the extra negation
       du[q] = __dsub_rn(__dmul_rn(E10.ey, dxR), __dmul_rn(E10.ex, dyR));
       bool inside = false;
-      if (QK == 1) {  // hull.cpp:80-90: discard iff cross > 0 for every edge
+      if (QK == 1 || QK == 3) {  // hull.cpp:80-90: discard iff no cross <= 0
         const double dxB = __dsub_rn(x, cxB), dyB = __dsub_rn(y, cyB);
         const double dxT = __dsub_rn(x, cxT), dyT = __dsub_rn(y, cyT);
-        inside = (xprod(Q[0].ex, Q[0].ey, dxL, dyL) > 0.0) &
-                 (xprod(Q[1].ex, Q[1].ey, dxB, dyB) > 0.0) &
-                 (xprod(Q[2].ex, Q[2].ey, dxR, dyR) > 0.0) &
-                 (xprod(Q[3].ex, Q[3].ey, dxT, dyT) > 0.0);
+        const double q0 = xprod(Q[0].ex, Q[0].ey, dxL, dyL), q1 = xprod(Q[1].ex, Q[1].ey, dxB, dyB);
+        const double q2 = xprod(Q[2].ex, Q[2].ey, dxR, dyR), q3 = xprod(Q[3].ex, Q[3].ey, dxT, dyT);
+        if (QK == 3)  // a wide box: a product may overflow and a cross be NaN, which the
+                      // reference's `cross <= 0` test counts as inside
+          inside = !(q0 <= 0.0) & !(q1 <= 0.0) & !(q2 <= 0.0) & !(q3 <= 0.0);
+        else          // every product is finite: no NaN, and > 0 is the same test
+          inside = (q0 > 0.0) & (q1 > 0.0) & (q2 > 0.0) & (q3 > 0.0);
       } else if (QK == 2) {  // degenerate quadrilateral (3 distinct corners)
         inside = true;
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq)
-          if (qq < ne) inside = inside & (cross_e(Q[qq], x, y) > 0.0);
+          if (qq < ne) inside = inside & !(cross_e(Q[qq], x, y) <= 0.0);
       }
       ins[q] = inside;
     }
@@ -529,7 +532,11 @@ __global__ void __launch_bounds__(Cfg2::TPB, 1) k2_classify(Bufs B) {
         tile(std::false_type{}, qk, s, first, cnt);
     }, pre);
   };
-  if (quad4)
+  // box extents below 2^500: every product of two coordinate differences is finite
+  const bool wide = !(((s_fin.e[2].x - s_fin.e[0].x) + (s_fin.e[3].y - s_fin.e[1].y)) < 0x1p500);
+  if (quad4 && wide)
+    pass(std::integral_constant<int, 3>{});
+  else if (quad4)
     pass(std::integral_constant<int, 1>{});
   else if (filt)
     pass(std::integral_constant<int, 2>{});
@@ -657,7 +664,7 @@ __global__ void __launch_bounds__(1024, 1) k_small_pre(Bufs B) {
       inside = valid;
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq)
-        if (qq < ne) inside = inside && (cross_e(Q[qq], x, y) > 0.0);
+        if (qq < ne) inside = inside && !(cross_e(Q[qq], x, y) <= 0.0);
     }
     const bool keep = valid && !inside;
     kept += keep;
@@ -824,7 +831,7 @@ __global__ void __launch_bounds__(KP_TPB) k_preprocess(Bufs B, double* ox, doubl
         bool inside = filt;  // hull.cpp:80-90: discard iff cross > 0 for every edge
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (k < ne) inside = inside & (cross_e(Q[k], px[j], py[j]) > 0.0);
+          if (k < ne) inside = inside & !(cross_e(Q[k], px[j], py[j]) <= 0.0);
         if (!inside) keep |= 1u << j;
       }
       const unsigned bal = __ballot_sync(FULL, (keep >> j) & 1u);

@@ -47,10 +47,18 @@ def shape(kind, n):
         bx, by = dataio.gen_uniform(max(1, n // 50), int(rng.integers(1 << 30)))
         k = rng.integers(0, bx.size, n)
         return bx[k].copy(), by[k].copy()
+    if kind == "offset":  # large coordinates, small extent (cancellation in every difference)
+        x, y = dataio.gen_uniform(n, int(rng.integers(1 << 30)))
+        return x + 1e8, y * 1e-3 - 3e7
+    if kind == "scaled":  # extreme magnitudes (the screen's range guards)
+        x, y = dataio.gen_uniform(n, int(rng.integers(1 << 30)))
+        f = [1e-300, 1e-100, 1e100, 1e300][int(rng.integers(4))]
+        return x * f, y * f
     raise ValueError(kind)
 
 
-kinds = ["uniform", "disk", "circle", "gauss", "clusters", "lattice", "line", "annulus", "dups"]
+kinds = ["uniform", "disk", "circle", "gauss", "clusters", "lattice", "line", "annulus", "dups",
+         "offset", "scaled"]
 bad = 0
 multi = 0
 multi_nonexact = 0
