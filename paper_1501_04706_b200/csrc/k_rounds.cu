@@ -628,13 +628,13 @@ constexpr int KR_U = LIVE_T / RCTHREADS;  // live points per consumer thread per
 #define SHB_MED 1
 #endif
 struct RoundSmem {
-  double2 lxy[LIVE_NS][LIVE_T];    // TMA ring of live points: xy          64 KB
-  uint2 lis[LIVE_NS][LIVE_T];      //                          (id, seg)   32 KB
-  unsigned long long lbar[LIVE_NS];   // full
-  unsigned long long lebar[LIVE_NS];  // empty (one arrival per warp)
+  double2 lxy[LIVE_NS][LIVE_T];    // TMA ring of live points: xy          90 KB
+  uint2 lis[LIVE_NS][LIVE_T];      //                          (id, seg)   45 KB
   Route rt[SMALL_S];               // route entries of a small table       32 KB
   unsigned long long db[NSLOT];    // CTA farthest slots: distance bits     8 KB
   SlotRec rec[NSLOT];              //                     records          32 KB
+  unsigned long long lbar[LIVE_NS];   // full   (after everything the solo tail overlays)
+  unsigned long long lebar[LIVE_NS];  // empty (one arrival per warp)
 };
 
 // medium tables reuse rt | db | rec (idle in large rounds) as one u64 array
@@ -697,7 +697,7 @@ SH_DEV void write_heads(const Bufs& B, uint32_t pin, uint32_t pout, const Route&
 // slots (a lone CTA kept them), the global records Srec (written by K3, the
 // small-input kernel or the solo tail), or the CTA rows of a multi-CTA round,
 // resolved through the winner words Wn.
-enum : uint32_t { RS_SMEM = 0, RS_SREC = 1, RS_ROWS = 2 };
+enum : uint32_t { RS_SMEM = 0, RS_SREC = 1, RS_ROWS = 2, RS_WIN = 3 };  // RS_WIN: solo import only
 struct RecSrc {
   uint32_t kind;
   const SlotRec* base;  // sm.rec, Srec[sin] or Rc[parity of the previous round]
@@ -986,50 +986,107 @@ SH_DEV bool table_large(const Bufs& B, uint32_t S, uint32_t Slo, uint32_t pin, u
 }
 
 // ---------------------------------------------------------------------------
-// Solo tail: once a single CTA is left with a small table and a live set that
-// fits its shared memory, it runs the remaining rounds with everything in
-// shared memory -- live points (ping-pong), head table, route table and
-// farthest records -- touching global memory only for the round stats and,
-// at the end, the final head table.  The ring's storage is reused.
-constexpr uint32_t SOLO_CAP = 2304;  // live points per ping-pong buffer
-static_assert(2 * SOLO_CAP + NSLOT <= (uint32_t)(LIVE_NS * LIVE_T), "solo tail does not fit the ring");
-static_assert(SMALL_S <= RTPB && 2 * SMALL_S <= NSLOT, "solo table: one segment per thread");
+// Solo tail: once a single CTA is left with a table of at most SOLO_S
+// segments and a live set that fits its shared memory, it runs the remaining
+// rounds with everything in shared memory -- live points (ping-pong), head
+// table, routes and farthest records -- touching global memory only for the
+// round stats and, at the end, the final head table.  It overlays the ring
+// and the small-table storage (everything in RoundSmem before the mbarriers).
+// Routes are compact: a point reads A, C and B from the new head table (A at
+// the segment's new index ns, C at ns + 1, B at ns + 2), which the table step
+// rewrites in place before the point step.
+constexpr uint32_t SOLO_S = 2 * RTPB;  // segments before a solo round (disk 20M: h = 933)
+constexpr uint32_t SOLO_NS = 2 * SOLO_S;
+constexpr uint32_t SOLO_CAP = 1512;    // live points per ping-pong buffer
+struct SoloSmem {
+  double2 pxy[2][SOLO_CAP];
+  uint2 pis[2][SOLO_CAP];          // (id, old segment)
+  double2 hxy[SOLO_NS];            // head table
+  uint32_t hid[SOLO_NS];
+  uint4 rt[SOLO_S];                // (new index ns, C's id, flags, -)
+  unsigned long long db[SOLO_NS];  // farthest records of the next round's segments
+  SlotRec rec[SOLO_NS];
+};
+static_assert(sizeof(SoloSmem) <= offsetof(RoundSmem, lbar), "solo tail does not fit");
+static_assert(offsetof(SoloSmem, rec) % 16 == 0 && offsetof(SoloSmem, hxy) % 16 == 0, "alignment");
 
 struct SoloState {
   uint32_t r, S, Slo, m, nruns;
 };
 
+// route_point for the solo tail's compact routes (the same rule)
+SH_DEV bool route_solo(const SoloSmem& so, uint32_t Sn, uint32_t seg, double x, double y, uint32_t id,
+                       double& d, uint32_t& nseg, bool& lower) {
+  const uint4 r = so.rt[seg];
+  lower = r.z & RT_LOWER;
+  nseg = r.x;
+  d = 0.0;
+  if (!(r.z & RT_SPLIT)) return false;
+  const uint32_t nb = r.x + 2 == Sn ? 0u : r.x + 2;
+  const double2 A = so.hxy[r.x], C = so.hxy[r.x + 1], Bv = so.hxy[nb];
+  const bool xeq = x == C.x;
+  const bool lt = x < C.x || (xeq && y < C.y);
+  const bool eq = xeq && y == C.y;
+  const bool left = lower ? lt : !(lt || eq);
+  const double2 S = left ? A : C, E = left ? C : Bv;
+  d = outward_e(make_edge(S.x, S.y, E.x, E.y), x, y);
+  nseg = r.x + (left ? 0u : 1u);
+  return id != r.y && d > 0.0;
+}
+
 // Returns true when the call is finished (control block written), false when
-// the table outgrew SMALL_S: the state is then exported to global memory (one
+// the table outgrew SOLO_S: the state is then exported to global memory (one
 // run, records in Srec) and the caller continues with the grid-wide rounds.
+// `rs` RS_WIN: the previous round used a large table (winner positions in Wn).
 SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSrc& rs,
                         uint32_t* s_ws, uint32_t* s_pref, uint32_t* s_off) {
   Ctl* c = B.ctl;
+  SoloSmem& so = *reinterpret_cast<SoloSmem*>(&sm.lxy[0][0]);
   const uint32_t tid = threadIdx.x, q = B.run_q, n = B.n;
-  double2* const buf_xy = &sm.lxy[0][0];
-  uint2* const buf_is = &sm.lis[0][0];
-  double2* const hxy = buf_xy + 2 * SOLO_CAP;  // head table (x, y)
-  uint2* const hid = buf_is + 2 * SOLO_CAP;    // head ids (.x)
   uint32_t r = st.r, S = st.S, Slo = st.Slo, m = st.m;
   const unsigned long long t0 = *(volatile unsigned long long*)&c->t0_ns;
-  {  // ---- import: heads, records (unless already here), live set ----
+  {  // ---- import: heads, records, live set ----
     const uint32_t pin = (r - 1) & 1u;
-    for (uint32_t s = tid; s < S; s += RTPB) {
-      hxy[s] = make_double2(__ldcg(B.Tx[pin] + s), __ldcg(B.Ty[pin] + s));
-      hid[s].x = __ldcg(B.Tid[pin] + s);
-      if (rs.kind != RS_SMEM) {
-        const SlotRec* g = rec_at(rs, s);
-        if (rec_id(g) == NONE) {
-          rec_clear(&sm.db[s], &sm.rec[s]);
-        } else {
-          sm.rec[s].d = __ldcg(&g->d);
-          sm.rec[s].x = __ldcg(&g->x);
-          sm.rec[s].y = __ldcg(&g->y);
-          sm.rec[s].id = __ldcg(&g->id);
-          sm.rec[s].lock = 0u;
-          sm.db[s] = (unsigned long long)__double_as_longlong(sm.rec[s].d);
+    // the records first, into registers: with RS_SMEM they sit in sm.rec,
+    // which the solo layout overlays
+    SlotRec g[SOLO_S / RTPB];
+#pragma unroll
+    for (int h = 0; h < (int)(SOLO_S / RTPB); ++h) {
+      const uint32_t s = tid + h * RTPB;
+      g[h].id = NONE;
+      g[h].d = g[h].x = g[h].y = 0.0;
+      g[h].lock = 0u;
+      if (s >= S) continue;
+      if (rs.kind == RS_SMEM) {
+        g[h] = sm.rec[s];
+      } else if (rs.kind == RS_WIN) {  // winner's live position (large table)
+        const uint32_t w = __ldcg(rs.wn + s);
+        if (w != NONE) {
+          const double2 v = __ldcg(B.Lxy[pin] + w);
+          g[h].x = v.x;
+          g[h].y = v.y;
+          g[h].id = __ldcg(&B.Lis[pin][w].x);
+          g[h].d = __longlong_as_double((long long)__ldcg(B.Sd[(r - 1) % 3u] + s));
+        }
+      } else {
+        const SlotRec* p = rec_at(rs, s);
+        if (rec_id(p) != NONE) {
+          g[h].d = __ldcg(&p->d);
+          g[h].x = __ldcg(&p->x);
+          g[h].y = __ldcg(&p->y);
+          g[h].id = __ldcg(&p->id);
         }
       }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < (int)(SOLO_S / RTPB); ++h) {
+      const uint32_t s = tid + h * RTPB;
+      if (s >= S) continue;
+      so.rec[s] = g[h];
+      so.db[s] = g[h].id == NONE ? 0ull : (unsigned long long)__double_as_longlong(g[h].d);
+      so.hxy[s] = make_double2(__ldcg(B.Tx[pin] + s), __ldcg(B.Ty[pin] + s));
+      so.hid[s] = __ldcg(B.Tid[pin] + s);
     }
     const uint32_t nruns = st.nruns;
     uint32_t tot;
@@ -1051,8 +1108,8 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
         if (s_pref[mid] <= v) a0 = mid; else a1 = mid;
       }
       const uint32_t phys = a0 * q + (v - s_pref[a0]);
-      buf_xy[v] = __ldcg(B.Lxy[pin] + phys);
-      buf_is[v] = __ldcg(B.Lis[pin] + phys);
+      so.pxy[0][v] = __ldcg(B.Lxy[pin] + phys);
+      so.pis[0][v] = __ldcg(B.Lis[pin] + phys);
     }
     m = Mp;  // entries of buffer 0, pads (segment NONE) included
     __syncthreads();
@@ -1060,48 +1117,60 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
   uint32_t cur = 0;
   while (true) {
     const uint32_t pout = r & 1u;
-    // ---- table: routes from heads + records, then the new heads in place ----
+    // ---- table: new indices and heads (in place), then the compact routes ----
     uint32_t Sn, Slon;
     {
-      uint32_t total;
-      const uint32_t s = tid;  // S <= SMALL_S <= RTPB
-      const bool split = s < S && sm.rec[s].id != NONE;
-      const uint32_t pre = block_exclusive_scan(split ? 1u : 0u, s_ws, &total);
-      const uint32_t lower_splits = (uint32_t)__syncthreads_count(split && s < Slo);
-      if (s < S) {
-        Route rr;
-        const double2 a = hxy[s], b = hxy[s + 1 == S ? 0u : s + 1];
-        rr.ax = a.x; rr.ay = a.y; rr.bx = b.x; rr.by = b.y;
-        rr.cx = split ? sm.rec[s].x : 0.0;
-        rr.cy = split ? sm.rec[s].y : 0.0;
-        rr.cid = split ? sm.rec[s].id : NONE;
-        rr.ns = s + pre;
-        rr.flags = (split ? RT_SPLIT : 0u) | (s < Slo ? RT_LOWER : 0u);
-        rr.pad = hid[s].x;  // A's id, for the new head table
-        sm.rt[s] = rr;
+      constexpr int H = SOLO_S / RTPB;
+      uint32_t ns[H], cid[H], fl[H];
+      double ax[H], ay[H], cx[H], cy[H];
+      uint32_t aid[H];
+      uint32_t running = 0, lower_splits = 0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const uint32_t s = tid + h * RTPB;
+        ns[h] = s;
+        fl[h] = 0u;
+        if (h > 0 && S <= (uint32_t)(h * RTPB)) continue;  // CTA-uniform: no segments here
+        const bool split = s < S && so.rec[s].id != NONE;
+        uint32_t total;
+        const uint32_t pre = block_exclusive_scan(split ? 1u : 0u, s_ws, &total);
+        lower_splits += (uint32_t)__syncthreads_count(split && s < Slo);
+        ns[h] = s + running + pre;
+        cid[h] = split ? so.rec[s].id : NONE;
+        fl[h] = (split ? RT_SPLIT : 0u) | (s < Slo ? RT_LOWER : 0u);
+        cx[h] = split ? so.rec[s].x : 0.0;
+        cy[h] = split ? so.rec[s].y : 0.0;
+        const double2 a = s < S ? so.hxy[s] : make_double2(0.0, 0.0);
+        ax[h] = a.x;
+        ay[h] = a.y;
+        aid[h] = s < S ? so.hid[s] : NONE;
+        running += total;
       }
-      Sn = S + total;
+      Sn = S + running;
       Slon = Slo + lower_splits;
-      __syncthreads();
-      if (s < S) {
-        const Route rr = sm.rt[s];
-        hxy[rr.ns] = make_double2(rr.ax, rr.ay);
-        hid[rr.ns].x = rr.pad;
-        if (rr.flags & RT_SPLIT) {
-          hxy[rr.ns + 1] = make_double2(rr.cx, rr.cy);
-          hid[rr.ns + 1].x = rr.cid;
+      __syncthreads();  // every old head and record is read
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const uint32_t s = tid + h * RTPB;
+        if (s >= S) continue;
+        so.rt[s] = make_uint4(ns[h], cid[h], fl[h], 0u);
+        so.hxy[ns[h]] = make_double2(ax[h], ay[h]);
+        so.hid[ns[h]] = aid[h];
+        if (fl[h] & RT_SPLIT) {
+          so.hxy[ns[h] + 1] = make_double2(cx[h], cy[h]);
+          so.hid[ns[h] + 1] = cid[h];
         }
       }
-      for (uint32_t t = tid; t < Sn; t += RTPB) rec_clear(&sm.db[t], &sm.rec[t]);
+      for (uint32_t t = tid; t < Sn; t += RTPB) rec_clear(&so.db[t], &so.rec[t]);
       if (tid == 0) *s_off = 0;
       __syncthreads();
     }
     const unsigned long long t_table = globaltimer_ns();
     // ---- points: route, keep, contend, append to the other buffer ----
-    const double2* ixy = buf_xy + cur * SOLO_CAP;
-    const uint2* iis = buf_is + cur * SOLO_CAP;
-    double2* oxy = buf_xy + (cur ^ 1u) * SOLO_CAP;
-    uint2* ois = buf_is + (cur ^ 1u) * SOLO_CAP;
+    const double2* ixy = so.pxy[cur];
+    const uint2* iis = so.pis[cur];
+    double2* oxy = so.pxy[cur ^ 1u];
+    uint2* ois = so.pis[cur ^ 1u];
     for (uint32_t i0 = 0; i0 < m; i0 += 2 * RTPB) {
       double px[2], py[2], pd[2];
       uint32_t pid[2], pseg[2];
@@ -1120,12 +1189,12 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
             px[u] = v.x;
             py[u] = v.y;
             pid[u] = is.x;
-            if (route_point<false>(sm.rt + is.y, v.x, v.y, is.x, pd[u], pseg[u], lower)) keepm |= 1u << u;
+            if (route_solo(so, Sn, is.y, v.x, v.y, is.x, pd[u], pseg[u], lower)) keepm |= 1u << u;
             if (lower) lowm |= 1u << u;
           }
         }
       }
-      contend_tile<2>(sm.db, sm.rec, keepm, px, py, pd, pid, pseg, lowm);
+      contend_tile<2>(so.db, so.rec, keepm, px, py, pd, pid, pseg, lowm);
       run_append<2>(keepm, px, py, pid, pseg, s_off, oxy, ois, 0u);
     }
     __syncthreads();
@@ -1143,13 +1212,13 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
       B.stats[r - 1] = sr;
     }
     const bool done = mn == 0 || r + 1 > n;
-    if (done || Sn > (uint32_t)SMALL_S) {
+    if (done || Sn > SOLO_S) {
       // ---- export: the head table (+ records and live set to continue) ----
       for (uint32_t t = tid; t < Sn; t += RTPB) {
-        const double2 h = hxy[t];
+        const double2 h = so.hxy[t];
         B.Tx[pout][t] = h.x;
         B.Ty[pout][t] = h.y;
-        B.Tid[pout][t] = hid[t].x;
+        B.Tid[pout][t] = so.hid[t];
       }
       if (done) {
         if (tid == 0) {
@@ -1166,12 +1235,12 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
       }
       const uint32_t sout = r % 3u;
       for (uint32_t t = tid; t < Sn; t += RTPB) {
-        B.Sd[sout][t] = sm.db[t];
+        B.Sd[sout][t] = so.db[t];
         SlotRec* g = B.Srec[sout] + t;
-        g->d = sm.rec[t].d;
-        g->x = sm.rec[t].x;
-        g->y = sm.rec[t].y;
-        g->id = sm.rec[t].id;
+        g->d = so.rec[t].d;
+        g->x = so.rec[t].x;
+        g->y = so.rec[t].y;
+        g->id = so.rec[t].id;
         g->lock = 0u;
       }
       for (uint32_t t = tid; t < mn + (mn & 1u); t += RTPB) {
@@ -1267,7 +1336,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
       P = want;
     }
     KR_MARK();  // round start
-    if (P == 1 && S <= (uint32_t)SMALL_S && m + nruns <= SOLO_CAP) {
+    if (P == 1 && S <= SOLO_S && m + nruns <= SOLO_CAP) {
       SoloState ss{r, S, Slo, m, nruns};
       const RecSrc rs0 = rec_src(rec_kind, r);
       if (solo_rounds(B, sm, ss, rs0, s_ws, s_pref, &s_off)) return;
@@ -1586,7 +1655,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     Slo = Slon;
     m = mn;
     nruns = P;
-    rec_kind = small ? (keep_smem ? RS_SMEM : RS_ROWS) : RS_SREC;
+    rec_kind = small ? (keep_smem ? RS_SMEM : RS_ROWS) : RS_WIN;
     prev_small = small;
     if (mn == 0 || r + 1 > n) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -17,6 +17,10 @@ from paper_1501_04706_b200 import dataio, hull  # noqa: E402
 k = float(os.environ.get("SCALE", "1"))  # racecheck is slow: SCALE=0.2
 cases = [("uniform", dataio.gen_uniform(int(2e6 * k), 3)), ("disk", dataio.gen_disk(int(1e6 * k), 3)),
          ("circle", dataio.gen_circle(int(1e6 * k), 3)), ("small", dataio.gen_uniform(5_000, 3))]
+# a 900-vertex hull over an interior disk: the solo tail with more than 512 segments
+_t = np.arange(900) * (2 * np.pi / 900)
+_ix, _iy = dataio.gen_disk(int(2e5 * k), 4)
+cases.append(("ring900", (np.concatenate([np.cos(_t), 0.99 * _ix]), np.concatenate([np.sin(_t), 0.99 * _iy]))))
 for name, (x, y) in cases:
     for mode in (1, 2):
         r = hull.run_arrays(x, y, mode)
