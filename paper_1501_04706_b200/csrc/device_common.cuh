@@ -297,6 +297,18 @@ SH_DEV uint32_t atom_add_relaxed(uint32_t* p, uint32_t v) {
   return old;
 }
 
+// (a CTA's shared slots keep only the high word of the distance bits: a
+// positive double's high word orders like the value, and 32-bit shared max is
+// a native atomic where the 64-bit one is a compare-and-swap loop)
+SH_DEV void rec_clear(uint32_t* dhi, SlotRec* rec) {
+  *dhi = 0u;
+  rec->d = 0.0;
+  rec->x = 0.0;
+  rec->y = 0.0;
+  rec->id = NONE;
+  rec->lock = 0u;
+}
+
 SH_DEV void rec_clear(unsigned long long* dbits, SlotRec* rec) {
   *dbits = 0ull;
   rec->d = 0.0;

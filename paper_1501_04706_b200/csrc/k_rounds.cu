@@ -179,21 +179,22 @@ SH_DEV void list_cands(uint32_t m, const unsigned long long (&db)[NP],
 }
 
 // Farthest-point contenders of a CTA with shared-memory slots (small tables):
-// a point that reaches the slot's running maximum (atomicMax on the distance
-// bits) settles the comparator under the record's lock.  After a CTA's first
-// tile almost no point passes the filter, so the lock is rare.
+// a point that reaches the slot's running maximum of the distance's high word
+// (native 32-bit shared atomicMax) settles the full comparator under the
+// record's lock.  After a CTA's first tile almost no point passes the filter,
+// so the lock is rare.
 template <int NP>
-SH_DEV void contend_tile(unsigned long long* s_db, SlotRec* s_rec, uint32_t keepm,
+SH_DEV void contend_tile(uint32_t* s_dh, SlotRec* s_rec, uint32_t keepm,
                          const double (&px)[NP], const double (&py)[NP],
                          const double (&pd)[NP], const uint32_t (&pid)[NP],
                          const uint32_t (&pseg)[NP], uint32_t lowm) {
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
     if ((keepm >> j) & 1u) {
-      const unsigned long long db = (unsigned long long)__double_as_longlong(pd[j]);
-      if (db >= *(volatile unsigned long long*)&s_db[pseg[j]]) {
-        const unsigned long long old = atomicMax(&s_db[pseg[j]], db);
-        if (db >= old) {
+      const uint32_t dh = (uint32_t)((unsigned long long)__double_as_longlong(pd[j]) >> 32);
+      if (dh >= *(volatile uint32_t*)&s_dh[pseg[j]]) {
+        const uint32_t old = atomicMax(&s_dh[pseg[j]], dh);
+        if (dh >= old) {
           Cand me;
           me.d = pd[j]; me.x = px[j]; me.y = py[j]; me.id = pid[j]; me.pos = 0;
           rec_update<true>(&s_rec[pseg[j]], me, (lowm >> j) & 1u);
@@ -207,7 +208,7 @@ SH_DEV void contend_tile(unsigned long long* s_db, SlotRec* s_rec, uint32_t keep
 // records go to its own row (plain stores), their distance bits to the
 // global running maxima (fire-and-forget atomicMax).  After the grid barrier,
 // claim_slots lets the rows that reached a slot's final maximum claim it.
-SH_DEV void flush_rows(const unsigned long long* s_db, const SlotRec* s_rec, uint32_t Sn,
+SH_DEV void flush_rows(const SlotRec* s_rec, uint32_t Sn,
                        unsigned long long* Sd, SlotRec* row) {
   for (uint32_t t = threadIdx.x; t < Sn; t += blockDim.x) {
     const volatile SlotRec* r = s_rec + t;
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
   typename L::Ring R;
   R.carve(smem_raw);
   __shared__ Route s_rt[2];
-  __shared__ unsigned long long s_db[4];
+  __shared__ uint32_t s_db[4];  // high words of the slots' running maxima
   __shared__ SlotRec s_rec[4];
   __shared__ uint32_t s_off, s_Sn, s_Slon;
   __shared__ int s_last;
@@ -503,9 +504,8 @@ __global__ void __launch_bounds__(Cfg3::TPB, 1) k3_round1(Bufs B) {
     uint32_t candm = 0;
 #pragma unroll
     for (int q = 0; q < K3_NP; ++q) {
-      const unsigned long long db = (unsigned long long)__double_as_longlong(pd[q]);
-      candm |= (uint32_t)(((keepm >> q) & 1u) &
-                          (db >= *(volatile unsigned long long*)&s_db[pseg[q] & 3u])) << q;
+      const uint32_t dh = (uint32_t)((unsigned long long)__double_as_longlong(pd[q]) >> 32);
+      candm |= (uint32_t)(((keepm >> q) & 1u) & (dh >= *(volatile uint32_t*)&s_db[pseg[q] & 3u])) << q;
     }
     if (__any_sync(FULL, candm)) contend_tile<K3_NP>(s_db, s_rec, candm, px, py, pd, pid, pseg, lowm);
     if (CAPPED)
@@ -631,7 +631,7 @@ struct RoundSmem {
   double2 lxy[LIVE_NS][LIVE_T];    // TMA ring of live points: xy          90 KB
   uint2 lis[LIVE_NS][LIVE_T];      //                          (id, seg)   45 KB
   Route rt[SMALL_S];               // route entries of a small table       32 KB
-  unsigned long long db[NSLOT];    // CTA farthest slots: distance bits     8 KB
+  uint32_t db[2 * NSLOT];          // CTA farthest slots: distance high words (first NSLOT) 8 KB
   SlotRec rec[NSLOT];              //                     records          32 KB
   unsigned long long lbar[LIVE_NS];   // full   (after everything the solo tail overlays)
   unsigned long long lebar[LIVE_NS];  // empty (one arrival per warp)
@@ -1004,7 +1004,7 @@ struct SoloSmem {
   double2 hxy[SOLO_NS];            // head table
   uint32_t hid[SOLO_NS];
   uint4 rt[SOLO_S];                // (new index ns, C's id, flags, -)
-  unsigned long long db[SOLO_NS];  // farthest records of the next round's segments
+  uint32_t db[SOLO_NS];            // farthest records of the next round's segments (high words)
   SlotRec rec[SOLO_NS];
 };
 static_assert(sizeof(SoloSmem) <= offsetof(RoundSmem, lbar), "solo tail does not fit");
@@ -1084,7 +1084,7 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
       const uint32_t s = tid + h * RTPB;
       if (s >= S) continue;
       so.rec[s] = g[h];
-      so.db[s] = g[h].id == NONE ? 0ull : (unsigned long long)__double_as_longlong(g[h].d);
+      so.db[s] = g[h].id == NONE ? 0u : (uint32_t)((unsigned long long)__double_as_longlong(g[h].d) >> 32);
       so.hxy[s] = make_double2(__ldcg(B.Tx[pin] + s), __ldcg(B.Ty[pin] + s));
       so.hid[s] = __ldcg(B.Tid[pin] + s);
     }
@@ -1235,7 +1235,7 @@ SH_DEV bool solo_rounds(const Bufs& B, RoundSmem& sm, SoloState& st, const RecSr
       }
       const uint32_t sout = r % 3u;
       for (uint32_t t = tid; t < Sn; t += RTPB) {
-        B.Sd[sout][t] = so.db[t];
+        B.Sd[sout][t] = so.rec[t].id == NONE ? 0ull : (unsigned long long)__double_as_longlong(so.rec[t].d);
         SlotRec* g = B.Srec[sout] + t;
         g->d = so.rec[t].d;
         g->x = so.rec[t].x;
@@ -1576,7 +1576,7 @@ __global__ void __launch_bounds__(RTPB, 1) k_rounds(Bufs B) {
     }
     // a lone CTA whose next table is small keeps its records in smem
     const bool keep_smem = small && P == 1 && Sn <= (uint32_t)SMALL_S;
-    if (small && !keep_smem) flush_rows(sm.db, sm.rec, Sn, Sd, B.Rc[r & 1u] + (size_t)blockIdx.x * NSLOT);
+    if (small && !keep_smem) flush_rows(sm.rec, Sn, Sd, B.Rc[r & 1u] + (size_t)blockIdx.x * NSLOT);
     if (threadIdx.x == 0) B.run_cnt[pout][blockIdx.x] = s_off;
     if (blockIdx.x == 0 && threadIdx.x == 0) t_points = globaltimer_ns();
     if (threadIdx.x == 0 && r == trace_r) B.dbg[blockIdx.x] = globaltimer_ns() - c->t0_ns;
