@@ -291,6 +291,15 @@ SH_DEV void rec_update(SlotRec* rec, const Cand& c, bool lower) {
 // relaxed gpu-scope atomic add issued from one lane: inline PTX so the
 // compiler cannot turn it into a warp-aggregated atomic whose result is
 // shuffled (and therefore waited for) right away
+// shared-memory atomic add from one lane: inline PTX, because the compiler
+// expands `if (lane == 0) atomicAdd(...)` into its warp-aggregation sequence
+// (vote, find-leader, popc, shuffle: ~15 instructions per call)
+SH_DEV uint32_t atom_add_shared(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+
 SH_DEV uint32_t atom_add_relaxed(uint32_t* p, uint32_t v) {
   uint32_t old;
   asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");

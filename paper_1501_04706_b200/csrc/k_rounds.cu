@@ -101,7 +101,7 @@ SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py
   }
   if (tot == 0) return;  // warp-uniform
   uint32_t off = 0;
-  if (lane == 0) off = atomicAdd(s_off, tot);
+  if (lane == 0) off = atom_add_shared(s_off, tot);
   off = base + __shfl_sync(FULL, off, 0);
   if (CAPPED && off + tot > lim) {  // warp-uniform
     if (lane == 0) *(volatile uint32_t*)ovf = ST_OVERFLOW;
@@ -127,7 +127,7 @@ SH_DEV void run_append(uint32_t keepm, const double (&px)[NP], const double (&py
       ctot += __popc(cb[j]);
     }
     uint32_t co = 0;
-    if (lane == 0) co = atomicAdd(s_coff, ctot);
+    if (lane == 0) co = atom_add_shared(s_coff, ctot);
     co = base + __shfl_sync(FULL, co, 0);
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
@@ -163,7 +163,7 @@ SH_DEV void list_cands(uint32_t m, const unsigned long long (&db)[NP],
     ctot += __popc(cb[j]);
   }
   uint32_t co = 0;
-  if (lane == 0) co = atomicAdd(s_coff, ctot);
+  if (lane == 0) co = atom_add_shared(s_coff, ctot);
   co = base + __shfl_sync(FULL, co, 0);
 #pragma unroll
   for (int j = 0; j < NP; ++j) {
