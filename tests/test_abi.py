@@ -96,3 +96,26 @@ def test_struct_layouts_match_header(tmp_path):
                                             check=True).stdout.split()]
     for n, c_size in zip(names, sizes):
         assert ctypes.sizeof(getattr(_lib, n)) == c_size, n
+
+
+def test_bench_reads_measured_peaks_layouts(tmp_path, monkeypatch):
+    """bench.py's roofline peak: the driver-written MEASURED_PEAKS.json in any of
+    the plausible layouts (sustained HBM preferred), else the profiling guide's
+    fallback -- never a silent wrong unit."""
+    import importlib.util
+    import json
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    monkeypatch.setattr(sys, "argv", ["bench.py"])
+    spec.loader.exec_module(bench)
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    assert bench.peaks() == (6650.0, "fallback")
+    for doc, want in [({"hbm_gbs": 6460.5}, 6460.5),
+                      ({"hbm": {"burst_gbs": 7000.0, "sustained_gbs": 6460.5}, "bf16_tflops": 1800}, 6460.5),
+                      ({"HBM_TBps": 6.46}, 6460.0)]:
+        (tmp_path / "MEASURED_PEAKS.json").write_text(json.dumps(doc))
+        v, kind = bench.peaks()
+        assert v == pytest.approx(want) and kind.startswith("measured")
